@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: one DPA-1 force evaluation per MD step (BASELINE.json north star).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--rc 6]
+                  [--weak] [--scheme masked|wide]
+
+* step     = one DpProvider::evaluate of the whole system: DD build, canonical neighbour
+             rows, DPA-1 forward + exact backward, force/virial assembly and (N > 1) the
+             NCCL force reduction -- the reference's dd_evaluate (decomp.cpp:265-542).
+* workload = configs[1]: 1HCI-sized synthetic solvated protein, 15,668 atoms, rho 0.1/A^3,
+             paper-sized DPA-1 (1,584,945 random-init params, seed 1), rc 6 A, n_max 160.
+             N > 1: the same system strong-scaled over N DD ranks (one per GPU); --weak
+             replicates it N times along x (cli.cpp:654-669).
+* value    = steps/s of the whole job, inputs resident in HBM, CUDA events on the
+             library's stream, max over ranks, L2 flushed (256 MB write) between steps.
+* e2e      = steps/s through the C-ABI host entry point (nnmd_b200_compute) from pinned
+             host buffers: H2D of coords/types/gids and D2H of energy/virial/forces/
+             per-atom energies inside the timed region (wall clock, max over ranks).
+* reference arm (--impl reference) = the compiled reference (oracle/_ref) on this box's
+             host cores: build_neighbor_list + a bounded sample of centres through
+             center_rows + evaluate_center (fwd + exact bwd) on all host threads,
+             extrapolated to the whole system (rank 0 only).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DT_FS = 2.0
+N_ATOMS = 15668
+RHO = 0.1
+
+
+def ns_per_day(steps_per_s):
+    return steps_per_s * 86400.0 * DT_FS * 1e-6
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def make_system(n_gpus, weak, seed=1):
+    import paper_2604_07276_b200 as nb
+    box, pos, sp = nb.synth_system(N_ATOMS, RHO, 0.9, seed)
+    if weak and n_gpus > 1:
+        reps = n_gpus
+        pos = np.concatenate([pos + np.array([k * box[0], 0.0, 0.0]) for k in range(reps)])
+        sp = np.concatenate([sp] * reps)
+        box = np.array([box[0] * reps, box[1], box[2]])
+    return box, np.ascontiguousarray(pos), np.ascontiguousarray(sp, dtype=np.int32)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    return ws, rank, local
+
+
+def allmax(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def bcast_bytes(b, ws):
+    if ws == 1:
+        return b
+    import torch
+    import torch.distributed as dist
+    t = torch.frombuffer(bytearray(b if b is not None else bytes(128)), dtype=torch.uint8).clone()
+    dist.broadcast(t, src=0)
+    return bytes(t.numpy().tobytes())
+
+
+# ---------------------------------------------------------------------------------------
+def cpu_reference_sample(box, pos, sp, rc, n_sample, seed=0):
+    """Compiled reference on host cores: neighbour list + n_sample centres (fwd+bwd)."""
+    import oracle as O
+    R = O.Ref()
+    spec = dict(O.PAPER_SPEC, rc=rc, rcs=0.55 * rc, n_max=O.nmax_for_rc(rc))
+    h = R.model_init(spec, 1)
+    rng = np.random.default_rng(seed)
+    centres = np.sort(rng.choice(len(pos), size=min(n_sample, len(pos)), replace=False)).astype(np.int32)
+    threads = host_threads()
+    t_list, t_cent, _ = R.time_centers(h, pos, sp, box, centres, threads)
+    R.model_free(h)
+    t_step = t_list + t_cent * len(pos) / len(centres)
+    return dict(value=1.0 / t_step, t_step=t_step, t_list=t_list, t_centres=t_cent, cores=threads,
+                sample=f"build_neighbor_list({len(pos)} atoms) + {len(centres)} random centres "
+                       f"(center_rows+evaluate_center, fwd+bwd) on {threads} threads, extrapolated x{len(pos)/len(centres):.1f}")
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    box, pos, sp = make_system(args.gpus, args.weak)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_sample(box, pos, sp, args.rc, args.ref_sample, seed=i)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = float(np.median(vals))
+    line = {"impl": "reference", "metric": "MD steps/s (DPA-1 force evaluation per step)", "value": v,
+            "unit": "steps/s", "higher_is_better": True, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / v, "ns_per_day": ns_per_day(v),
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic solvated protein (nnmd_synth_system), random-init DPA-1 weights",
+            "config": {"workload": f"1HCI-sized {len(pos)} atoms, DPA-1 1.58M params, rc={args.rc}",
+                       "n_atoms": len(pos), "rc": args.rc},
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": r["cores"], "kind": "reference",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+def algorithmic_flops(counts):
+    """SURVEY 8(d) per-centre work of the reference algorithm (MACs -> x2 FLOP).
+    centre_backward (dominant kernel): B(n) minus the fitting net, run in k_fit."""
+    n = counts.astype(np.float64)
+    fwd = 2.0 * (404640 * n + 1548 * n * n + 1196288 - 1179904)
+    bwd = 2.0 * (405280 * n + 3084 * n * n + 1212672 - 1179904)
+    return fwd.sum(), bwd.sum()
+
+
+def executed_flops(counts, M=128, E=(32, 64), na=3):
+    """FLOPs the folded kernels execute (attention re-associated; SIMT, no padding)."""
+    n = counts.astype(np.float64)
+    emb = n * (E[0] * E[1] + E[1] * M)
+    att_f = na * (n * M * 2 * M + 2 * n * n * M)
+    att_b = na * (n * M * 2 * M + 2 * n * n * M) + na * (4 * n * n * M + n * 2 * M * M)
+    return 2 * (emb + att_f).sum(), 2 * (2 * emb + att_b).sum()
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2604_07276_b200 as nb
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    box, pos, sp = make_system(args.gpus, args.weak)
+    n = len(pos)
+    model = nb.init_model(nb.paper_spec(args.rc), 1)
+    uid = nb.DeviceEvaluator.nccl_unique_id() if (ws > 1 and rank == 0) else None
+    uid = bcast_bytes(uid, ws) if ws > 1 else None
+    scheme = nb.WIDE_HALO if args.scheme == "wide" else nb.MASKED_REDUCTION
+    ev = nb.DeviceEvaluator(model, n_ranks=ws, scheme=scheme, device=local, world_size=ws, world_rank=rank,
+                            nccl_id=uid)
+    stream = torch.cuda.ExternalStream(ev.stream(), device=dev)
+    d_pos = torch.from_numpy(pos).to(dev)
+    d_sp = torch.from_numpy(sp).to(dev)
+    d_gid = torch.arange(n, dtype=torch.int64, device=dev)
+    d_out = torch.zeros(10 + 4 * n, dtype=torch.float64, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    torch.cuda.synchronize()
+
+    def step():
+        ev.compute_device(n, d_pos.data_ptr(), d_sp.data_ptr(), d_gid.data_ptr(), box, d_out.data_ptr())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = nb.lib().nnmd_b200_launch_count()
+    ev_times = []
+    kernel_acc = {}
+    with ClockSampler(local) as clk:
+        barrier(ws)
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            step()
+            b.record(stream)
+            b.synchronize()
+            ev_times.append(a.elapsed_time(b))
+            for name, ms in ev.kernel_times():
+                kernel_acc[name] = kernel_acc.get(name, 0.0) + ms
+        torch.cuda.synchronize()
+        barrier(ws)
+    launches = nb.lib().nnmd_b200_launch_count() - launches0
+    ms_step = allmax(float(np.mean(ev_times)), ws)
+    value = 1000.0 / ms_step
+    stats = ev.rank_stats(rank)
+    clocks = clk.summary()
+
+    # ---- roofline of the dominant kernel (centre_backward), per launch
+    res = d_out[10:10 + 3 * n].cpu()
+    ev.set_debug(True)
+    step()
+    _, _, _, cnt = ev.debug_nlist(rank, nb.paper_spec(args.rc).n_max)
+    ev.set_debug(False)
+    f_fwd, f_bwd = algorithmic_flops(cnt)
+    x_fwd, x_bwd = executed_flops(cnt)
+    k_bwd = kernel_acc.get("centre_backward", 0.0) / args.steps
+    k_fwd = kernel_acc.get("centre_forward", 0.0) / args.steps
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("bf16_tflops_sustained", 1366.3)
+    achieved = f_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0
+
+    # ---- e2e through the host C-ABI entry point (pinned host buffers)
+    h_pos = torch.from_numpy(pos).pin_memory().numpy()
+    h_sp = torch.from_numpy(sp).pin_memory().numpy()
+    h_gid = torch.arange(n, dtype=torch.int64).pin_memory().numpy()
+    for _ in range(max(1, args.warmup)):
+        ev.compute(h_pos, h_sp, box, gids=h_gid)
+    barrier(ws)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = ev.compute(h_pos, h_sp, box, gids=h_gid)
+    t_e2e = allmax((time.perf_counter() - t0) / args.steps, ws)
+    e2e = 1.0 / t_e2e
+    h2d = ws * n * (24 + 4 + 8)
+    d2h = ws * (8 * 10 + n * 24 + n * 8)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        c = cpu_reference_sample(box, pos, sp, args.rc, args.ref_sample)
+        cpu = {"value": c["value"], "unit": "steps/s", "cores": c["cores"], "kind": "reference", "sample": c["sample"]}
+
+    if rank == 0:
+        line = {
+            "metric": "MD steps/s (DPA-1 force evaluation per step)", "value": value, "unit": "steps/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic solvated protein (nnmd_synth_system seed 1), random-init DPA-1 weights (init_model seed 1)",
+            "ns_per_day": ns_per_day(value),
+            "config": {"workload": f"1HCI-sized solvated protein, {n} atoms, DPA-1 1.58M params, rc={args.rc} A, "
+                                   f"{'weak' if args.weak else 'strong'} DD over {ws} GPU(s)",
+                       "n_atoms": n, "rc": args.rc, "n_max": nb.paper_spec(args.rc).n_max,
+                       "dd_ranks": ws, "scheme": args.scheme, "l2": "flushed between steps (256 MB write)",
+                       "precision": "fp32 network (SIMT), fp64 geometry/forces"},
+            "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ns_per_day": ns_per_day(e2e)},
+            "roofline": {"bound": "tensor", "kernel": "k_centre_backward", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "algorithmic_flop_per_launch": f_bwd, "ms_per_launch": k_bwd,
+                         "executed_tflops": x_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                         "forward": {"ms_per_launch": k_fwd, "algorithmic_flop": f_fwd,
+                                     "achieved_tflops": f_fwd / (k_fwd * 1e-3) / 1e12 if k_fwd > 0 else 0.0}},
+            "kernel_ms_per_step": {k: v / args.steps for k, v in sorted(kernel_acc.items(), key=lambda x: -x[1])},
+            "rank0_stats": stats,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "energy": float(d_out[0].item()),
+        }
+        print(json.dumps(line), flush=True)
+    ev.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--rc", type=float, default=6.0)
+    ap.add_argument("--weak", action="store_true")
+    ap.add_argument("--scheme", choices=["masked", "wide"], default="masked")
+    ap.add_argument("--ref-sample", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

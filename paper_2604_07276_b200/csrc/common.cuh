@@ -1,0 +1,77 @@
+// Shared device helpers for the nnmd_b200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nb {
+
+constexpr int kWarp = 32;
+
+// Packed image shift: (sx+1)*9 + (sy+1)*3 + (sz+1), 13 == zero shift.
+__host__ __device__ inline int pack_shift(int sx, int sy, int sz) {
+  return (sx + 1) * 9 + (sy + 1) * 3 + (sz + 1);
+}
+__host__ __device__ inline int shift_x(int p) { return p / 9 - 1; }
+__host__ __device__ inline int shift_y(int p) { return (p / 3) % 3 - 1; }
+__host__ __device__ inline int shift_z(int p) { return p % 3 - 1; }
+constexpr int kZeroShift = 13;
+
+// ---- exact FP64 arithmetic of the reference geometry (no FMA contraction) -----------
+// image_delta(rj, ri, s, L) = (rj - ri) + s*L   (vec.hpp:52-54)
+__device__ __forceinline__ double image_delta(double rj, double ri, int s, double L) {
+  return __dadd_rn(__dsub_rn(rj, ri), __dmul_rn(static_cast<double>(s), L));
+}
+// norm2 = (x*x + y*y) + z*z   (vec.hpp:28-31)
+__device__ __forceinline__ double norm2_exact(double x, double y, double z) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
+}
+
+// switch_eval (dp_core.hpp:116-137), FP64
+__device__ __forceinline__ void switch_fn(double r, double rcs, double rc, double& s, double& ds) {
+  if (r >= rc) {
+    s = 0.0;
+    ds = 0.0;
+    return;
+  }
+  const double inv = 1.0 / r;
+  if (r <= rcs) {
+    s = inv;
+    ds = -inv * inv;
+    return;
+  }
+  const double span = rc - rcs;
+  const double u = (r - rcs) * (1.0 / span);
+  const double u2 = u * u, u3 = u2 * u;
+  const double w = u3 * (u * (-6.0 * u + 15.0) - 10.0) + 1.0;
+  const double dw = -30.0 * u2 * (u - 1.0) * (u - 1.0) * (1.0 / span);
+  s = w * inv;
+  ds = dw * inv - w * inv * inv;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block reduction of a double (fixed tree), result valid in all threads.
+// scratch: >= blockDim.x/32 doubles of shared memory.
+__device__ __forceinline__ double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += scratch[w];
+  __syncthreads();
+  return t;
+}
+
+}  // namespace nb

@@ -1,0 +1,598 @@
+// nnmd_b200 device context: one DpProvider::evaluate / dd_evaluate step on a B200.
+//
+// Per step (reference dd_evaluate, decomp.cpp:265-542):
+//   ownership (+ input validation)                      k_owner
+//   for each DD rank handled by this process (ascending):
+//     halo slab test, locals/ghosts compaction           k_dd_flags, k_scan, k_dd_members
+//     centres (locals [+ first-layer ghosts, wide])      k_centre_flags, k_scan, k_centre_compact
+//     cell grid over member images                       k_cell_count, k_scan, k_cell_fill
+//     canonical neighbour rows (+ ghost reverse lists)   k_neighbors
+//     DPA-1 forward / fit / exact backward               k_centre_forward, k_fit_*, k_centre_backward
+//     deterministic force gather + per-atom assembly     k_force_gather, k_assemble, k_energy_virial
+//   cross-process force/energy/virial reduction          ncclAllReduce (world_size > 1)
+// One host read-back per rank (the DD-build counts, to size the rest of the step).
+#include "context.h"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+namespace nb {
+
+#define CU(x)                                                                               \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+static inline int shift_x_host(int p) { return p / 9 - 1; }
+static inline int shift_y_host(int p) { return (p / 3) % 3 - 1; }
+static inline int shift_z_host(int p) { return p % 3 - 1; }
+
+static void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+void DevBuf<T>::ensure(size_t n) {
+  if (p && n <= cap) return;
+  release();
+  const size_t c = std::max<size_t>(n + n / 4, 64);
+  CU(cudaMalloc(reinterpret_cast<void**>(&p), c * sizeof(T)));
+  cap = c;
+}
+template <class T>
+void DevBuf<T>::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+template struct DevBuf<int>;
+template struct DevBuf<float>;
+template struct DevBuf<float4>;
+template struct DevBuf<double>;
+template struct DevBuf<int64_t>;
+
+// partition_ranks (decomp.cpp:17-57): minimise subdomain surface; ties -> most balanced
+// (sorted-descending dims smallest), then lexicographically largest dims.
+std::vector<int> partition_ranks(const double L[3], int R, double min_edge) {
+  require(R >= 1, "partition_ranks: n_ranks must be >= 1");
+  bool have = false;
+  std::vector<int> best(3), best_sorted(3);
+  double best_surf = 0;
+  for (int px = 1; px <= R; ++px) {
+    if (R % px) continue;
+    for (int py = 1; py <= R / px; ++py) {
+      if ((R / px) % py) continue;
+      const int pz = R / px / py;
+      const double a = L[0] / px, b = L[1] / py, c = L[2] / pz;
+      if (std::min({a, b, c}) < min_edge) continue;
+      const double surf = 2.0 * (a * b + b * c + c * a);
+      std::vector<int> dims{px, py, pz}, srt = dims;
+      std::sort(srt.begin(), srt.end(), std::greater<int>());
+      if (!have || surf < best_surf ||
+          (surf == best_surf && (srt < best_sorted || (srt == best_sorted && dims > best)))) {
+        have = true;
+        best = dims;
+        best_sorted = srt;
+        best_surf = surf;
+      }
+    }
+  }
+  require(have, "partition_ranks: no factorization of " + std::to_string(R) +
+                    " ranks fits the halo constraints of this box; use a smaller rank count");
+  return best;
+}
+
+Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) {
+  model_.validate();
+  require(o.n_ranks >= 1, "nnmd_b200: n_ranks must be >= 1");
+  require(o.scheme == NNMD_MASKED_REDUCTION || o.scheme == NNMD_WIDE_HALO, "nnmd_b200: bad scheme");
+  require(o.precision == NNMD_PREC_FP32, "nnmd_b200: unsupported precision");
+  require(o.world_size >= 1 && o.world_rank >= 0 && o.world_rank < o.world_size,
+          "nnmd_b200: bad world_size/world_rank");
+  require(model_.na <= 16 && model_.embed.size() <= kMaxLayers && model_.fit.size() <= kMaxLayers,
+          "nnmd_b200: at most 16 attention layers and 8 layers per MLP");
+  CU(cudaSetDevice(o.device));
+  CU(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, o.device));
+  n_sm_ = prop.multiProcessorCount;
+  wh_ = fold_weights(model_);
+  weights_.ensure(wh_.blob.size());
+  CU(cudaMemcpy(weights_.p, wh_.blob.data(), wh_.blob.size() * sizeof(float), cudaMemcpyHostToDevice));
+  CU(cudaMallocHost(reinterpret_cast<void**>(&h_counts_), 64 * sizeof(int)));
+  require(o.n_ranks <= 48, "nnmd_b200: at most 48 DD ranks");
+  stats_.resize(static_cast<size_t>(o.n_ranks));
+  debug_.resize(static_cast<size_t>(o.n_ranks));
+  if (o.world_size > 1) {
+    const Nccl& N = nccl();
+    require(N.ok, "nnmd_b200: NCCL unavailable: " + N.err);
+    require(o.nccl_id != nullptr, "nnmd_b200: world_size > 1 needs an nccl_id");
+    NcclUid uid;
+    std::memcpy(&uid, o.nccl_id, sizeof uid);
+    const int r = N.CommInitRank(&comm_, o.world_size, uid, o.world_rank);
+    if (r != 0) throw CudaError(std::string("ncclCommInitRank: ") + N.GetErrorString(r));
+  }
+}
+
+Context::~Context() {
+  if (comm_) nccl().CommDestroy(comm_);
+  for (auto e : pool_) cudaEventDestroy(e);
+  if (h_counts_) cudaFreeHost(h_counts_);
+  if (h_out_) cudaFreeHost(h_out_);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void Context::tic(const char* name) {
+  if (pool_used_ + 2 > pool_.size()) {
+    for (int i = 0; i < 32; ++i) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      pool_.push_back(e);
+    }
+  }
+  Timer t{name, pool_[pool_used_], pool_[pool_used_ + 1]};
+  pool_used_ += 2;
+  CU(cudaEventRecord(t.a, st_));
+  timers_.push_back(t);
+}
+
+void Context::toc() {
+  check_launch(timers_.back().name.c_str());
+  CU(cudaEventRecord(timers_.back().b, st_));
+}
+
+void Context::collect_times() {
+  ktimes_.clear();
+  for (const auto& t : timers_) {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, t.a, t.b));
+    ktimes_.push_back({t.name, ms});
+  }
+  for (const auto& ph : phases_) {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, timers_[ph.t0].a, timers_[ph.t1].b));
+    stats_[static_cast<size_t>(ph.rank)].ms[ph.phase] += ms;
+  }
+}
+
+void Context::compute_device(long n, const double* d_pos, const int* d_types,
+                             const int64_t* d_gid, const double box[3],
+                             const uint8_t periodic[3], double* d_out) {
+  const Model& m = model_;
+  require(n >= 0 && n < INT_MAX / 32, "nnmd_b200: bad atom count");
+  for (int a = 0; a < 3; ++a) {
+    require(box[a] > 0.0, "SimBox: non-positive edge length");
+    if (periodic[a])
+      require(box[a] >= 2.0 * m.rc, "SimBox: periodic edge shorter than 2*rc (minimum image invalid)");
+  }
+  const bool wide = opts_.scheme == NNMD_WIDE_HALO;
+  const double thickness = wide ? 2.0 * m.rc : m.rc;
+  const std::vector<int> dims = partition_ranks(box, opts_.n_ranks, thickness);
+  for (int a = 0; a < 3; ++a) {
+    require(box[a] / dims[a] >= thickness, "dd_evaluate: subdomain edge shorter than the halo thickness");
+    require(!periodic[a] || thickness <= box[a],
+            "build_halo: thickness exceeds the box (single image layer insufficient)");
+  }
+  timers_.clear();
+  phases_.clear();
+  pool_used_ = 0;
+  for (auto& s : stats_) s = RankStat{};
+  const size_t out_len = 10 + 4 * static_cast<size_t>(n);
+  CU(cudaMemsetAsync(d_out, 0, out_len * sizeof(double), st_));
+  owner_.ensure(static_cast<size_t>(n) + 1);
+  err_.ensure(8);
+  CU(cudaMemsetAsync(err_.p, 0x7f, 8 * sizeof(int), st_));
+  SysArgs sys{};
+  sys.pos = d_pos;
+  sys.species = d_types;
+  sys.gid = d_gid;
+  sys.n = static_cast<int>(n);
+  sys.n_species = m.ns;
+  for (int a = 0; a < 3; ++a) {
+    sys.L[a] = box[a];
+    sys.per[a] = periodic[a] ? 1 : 0;
+  }
+  tic("owner");
+  launch_owner(sys, dims.data(), owner_.p, err_.p, st_);
+  toc();
+  for (int r = 0; r < opts_.n_ranks; ++r)
+    if (r % opts_.world_size == opts_.world_rank) run_rank(r, sys, dims.data(), thickness, d_out, keep_debug_);
+  if (opts_.world_size > 1) {
+    tic("nccl_allreduce");
+    const Nccl& N = nccl();
+    const int rc = N.AllReduce(d_out, d_out, out_len, kNcclFloat64, kNcclSum, comm_, st_);
+    if (rc != 0) throw CudaError(std::string("ncclAllReduce: ") + N.GetErrorString(rc));
+    toc();
+  }
+  CU(cudaMemcpyAsync(h_counts_ + 8, err_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CU(cudaStreamSynchronize(st_));
+  collect_times();
+  if (opts_.scheme == NNMD_MASKED_REDUCTION)
+    for (int r = 0; r < opts_.n_ranks; ++r)
+      if (r % opts_.world_size == opts_.world_rank) stats_[static_cast<size_t>(r)].counts[3] = h_counts_[16 + (r % 48)];
+  if (opts_.world_size > 1) {
+    const double comm = ktimes_.back().second;
+    for (auto& s : stats_) s.ms[3] += comm;
+  }
+  if (h_counts_[9] != 0x7f7f7f7f || h_counts_[10] != 0x7f7f7f7f) {
+    const int atom = std::min(h_counts_[9], h_counts_[10]);
+    int64_t gid = atom;
+    if (d_gid) CU(cudaMemcpy(&gid, d_gid + atom, sizeof gid, cudaMemcpyDeviceToHost));
+    int own = 0;
+    CU(cudaMemcpy(&own, owner_.p + atom, sizeof own, cudaMemcpyDeviceToHost));
+    throw CapacityError("dd_evaluate: neighbor overflow at atom id " + std::to_string(gid) +
+                        " on rank " + std::to_string(own) + " (n_max " + std::to_string(m.n_max) + ")");
+  }
+}
+
+void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double thickness,
+                       double* d_out, bool keep_debug) {
+  const Model& m = model_;
+  const int n = sys.n;
+  const bool wide = opts_.scheme == NNMD_WIDE_HALO;
+  RankArgs ra{};
+  ra.rank = rank;
+  ra.wide = wide;
+  const int idx[3] = {rank / (dims[1] * dims[2]), (rank / dims[2]) % dims[1], rank % dims[2]};
+  for (int a = 0; a < 3; ++a) {
+    ra.dims[a] = dims[a];
+    const double edge = sys.L[a] / dims[a];
+    ra.lo[a] = idx[a] * edge;
+    ra.hi[a] = (idx[a] + 1) * edge;
+    const double guard = 1e-12 * sys.L[a];  // kHaloSlabGuard (decomp.hpp:55)
+    ra.slab_lo[a] = ra.lo[a] - thickness - guard;
+    ra.slab_hi[a] = ra.hi[a] + thickness + guard;
+    ra.rc_lo[a] = ra.lo[a] - m.rc - guard;
+    ra.rc_hi[a] = ra.hi[a] + m.rc + guard;
+  }
+  RankStat& stat = stats_[static_cast<size_t>(rank)];
+  const size_t ph_dd0 = timers_.size();
+
+  // ---- DD build: locals + halo ------------------------------------------------------
+  is_local_.ensure(n + 1);
+  gcount_.ensure(n + 1);
+  loc_off_.ensure(n + 1);
+  gh_off_.ensure(n + 1);
+  counts_.ensure(8);
+  tic("dd_flags");
+  launch_dd_flags(sys, ra, owner_.p, is_local_.p, gcount_.p, st_);
+  toc();
+  tic("scan");
+  launch_scan(is_local_.p, loc_off_.p, n, st_);
+  launch_scan(gcount_.p, gh_off_.p, n, st_);
+  toc();
+  CU(cudaMemsetAsync(counts_.p, 0, 8 * sizeof(int), st_));
+  CU(cudaMemcpyAsync(counts_.p + 0, loc_off_.p + n, sizeof(int), cudaMemcpyDeviceToDevice, st_));
+  CU(cudaMemcpyAsync(counts_.p + 1, gh_off_.p + n, sizeof(int), cudaMemcpyDeviceToDevice, st_));
+  CU(cudaMemcpyAsync(h_counts_, counts_.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CU(cudaMemcpyAsync(h_counts_ + 4, err_.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CU(cudaStreamSynchronize(st_));
+  if (h_counts_[4] != 0x7f7f7f7f) {
+    const int atom = h_counts_[4];
+    int sp = 0;
+    double p[3];
+    CU(cudaMemcpy(&sp, sys.species + atom, sizeof sp, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(p, sys.pos + 3 * static_cast<size_t>(atom), sizeof p, cudaMemcpyDeviceToHost));
+    if (sp < 0 || sp >= m.ns) throw Error("dd_evaluate: species id outside the model's species table");
+    throw Error("neighbor list: positions must be wrapped into [0, L) on periodic axes");
+  }
+  const int nloc = h_counts_[0], ngh = h_counts_[1], nm = nloc + ngh;
+  m_atom_.ensure(nm + 1);
+  m_shift_.ensure(nm + 1);
+  m_owner_.ensure(nm + 1);
+  m_pos_.ensure(3 * static_cast<size_t>(nm) + 3);
+  m_cell_.ensure(nm + 1);
+  cflag_.ensure(nm + 1);
+  coff_.ensure(nm + 1);
+  cen_member_.ensure(nm + 1);
+  cidx_.ensure(nm + 1);
+  tic("dd_members");
+  launch_dd_members(sys, ra, owner_.p, loc_off_.p, gh_off_.p, n, m_atom_.p, m_shift_.p, m_pos_.p,
+                    m_owner_.p, st_);
+  launch_centre_flags(ra, counts_.p, m_pos_.p, nm, cflag_.p, st_);
+  launch_scan(cflag_.p, coff_.p, nm, st_);
+  launch_centre_compact(cflag_.p, coff_.p, nm, cen_member_.p, cidx_.p, st_);
+  toc();
+  int ncen = nloc;
+  if (wide) {
+    CU(cudaMemcpyAsync(h_counts_ + 2, coff_.p + nm, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    CU(cudaStreamSynchronize(st_));
+    ncen = h_counts_[2];
+  }
+  stat.counts[0] = nloc;
+  stat.counts[1] = ngh;
+  stat.counts[2] = ncen;
+  phases_.push_back({rank, 0, ph_dd0, timers_.size() - 1});
+
+  // ---- cell grid + neighbour rows ------------------------------------------------------
+  const size_t ph_nb0 = timers_.size();
+  CellArgs cg{};
+  long ncell = 1;
+  for (int a = 0; a < 3; ++a) {
+    const double ext = ra.slab_hi[a] - ra.slab_lo[a];
+    cg.origin[a] = ra.slab_lo[a];
+    cg.dims[a] = std::max(1, std::min(1024, static_cast<int>(std::floor(ext / (m.rc * (1.0 + 1e-6))))));
+    cg.width[a] = ext / cg.dims[a];
+    ncell *= cg.dims[a];
+  }
+  cell_count_.ensure(ncell + 1);
+  cell_start_.ensure(ncell + 1);
+  cell_fill_.ensure(ncell + 1);
+  cell_members_.ensure(nm + 1);
+  tic("cells");
+  CU(cudaMemsetAsync(cell_count_.p, 0, (ncell + 1) * sizeof(int), st_));
+  CU(cudaMemsetAsync(cell_fill_.p, 0, (ncell + 1) * sizeof(int), st_));
+  launch_cell_count(cg, m_pos_.p, nm, m_cell_.p, cell_count_.p, st_);
+  launch_scan(cell_count_.p, cell_start_.p, static_cast<int>(ncell), st_);
+  launch_cell_fill(m_cell_.p, nm, cell_start_.p, cell_fill_.p, cell_members_.p, st_);
+  toc();
+  const int nmax = m.n_max;
+  nlist_.ensure(static_cast<size_t>(ncen) * nmax + 1);
+  nn_.ensure(ncen + 1);
+  NbrArgs na{};
+  na.pos = sys.pos;
+  na.species = sys.species;
+  na.gid = sys.gid;
+  for (int a = 0; a < 3; ++a) {
+    na.L[a] = sys.L[a];
+    na.cdims[a] = cg.dims[a];
+  }
+  na.m_atom = m_atom_.p;
+  na.m_shift = m_shift_.p;
+  na.m_cell = m_cell_.p;
+  na.cell_start = cell_start_.p;
+  na.cell_members = cell_members_.p;
+  na.n_max = nmax;
+  na.rc2 = m.rc * m.rc;
+  na.centre_member = cen_member_.p;
+  na.n_lists = ncen;
+  na.cand_limit = INT_MAX;
+  na.nlist = nlist_.p;
+  na.nn = nn_.p;
+  na.err = err_.p + 1;
+  na.nonempty = nullptr;
+  tic("neighbors");
+  launch_neighbors(na, st_);
+  toc();
+  if (!wide) {
+    rlist_.ensure(static_cast<size_t>(ngh) * nmax + 1);
+    rn_.ensure(ngh + 1);
+    NbrArgs rv = na;
+    rv.centre_member = nullptr;
+    rv.member_offset = nloc;
+    rv.n_lists = ngh;
+    rv.cand_limit = nloc;
+    rv.nlist = rlist_.p;
+    rv.nn = rn_.p;
+    rv.err = err_.p + 2;
+    rv.nonempty = counts_.p + 3;
+    tic("neighbors_reverse");
+    launch_neighbors(rv, st_);
+    toc();
+  }
+  phases_.push_back({rank, 1, ph_nb0, timers_.size() - 1});
+
+  // ---- network -------------------------------------------------------------------------
+  const size_t ph_in0 = timers_.size();
+  const int M = m.M, mr = m.mr;
+  DpArgs dp{};
+  dp.M = M;
+  dp.mr = mr;
+  dp.n_max = nmax;
+  dp.ns = m.ns;
+  dp.n_embed = static_cast<int>(m.embed.size());
+  dp.n_attn = m.na;
+  dp.n_fit = static_cast<int>(m.fit.size());
+  const float* W = weights_.p;
+  for (int e = 0; e < dp.n_embed; ++e) {
+    dp.edims[e] = wh_.edims[static_cast<size_t>(e)];
+    dp.ew[e] = e ? W + wh_.ew[static_cast<size_t>(e)] : nullptr;
+    dp.eb[e] = e ? W + wh_.eb[static_cast<size_t>(e)] : nullptr;
+  }
+  dp.w0 = W + wh_.w0;
+  dp.ctab = W + wh_.ctab;
+  for (int l = 0; l < m.na; ++l) dp.ab[l] = W + wh_.ab[static_cast<size_t>(l)];
+  for (int l = 0; l <= dp.n_fit; ++l) dp.fdims[l] = wh_.fdims[static_cast<size_t>(l)];
+  for (int l = 0; l < dp.n_fit; ++l) {
+    dp.fw[l] = W + wh_.fw[static_cast<size_t>(l)];
+    dp.fb[l] = W + wh_.fb[static_cast<size_t>(l)];
+  }
+  dp.rc = m.rc;
+  dp.rcs = m.rcs;
+  dp.inv_sqrt_nmax = static_cast<float>(1.0 / std::sqrt(static_cast<double>(nmax)));
+  dp.pos = sys.pos;
+  dp.species = sys.species;
+  for (int a = 0; a < 3; ++a) dp.L[a] = sys.L[a];
+  dp.m_atom = m_atom_.p;
+  dp.m_shift = m_shift_.p;
+  dp.cen_member = cen_member_.p;
+  dp.n_centres = ncen;
+  dp.nlist = nlist_.p;
+  dp.nn = nn_.p;
+  dp.x_layer_stride = static_cast<size_t>(ncen) * nmax * M;
+  X_.ensure(dp.x_layer_stride * (m.na + 1) + 4);
+  R_.ensure(static_cast<size_t>(ncen) * nmax + 1);
+  Ad_.ensure(static_cast<size_t>(ncen) * M * 4 + 4);
+  Bd_.ensure(static_cast<size_t>(ncen) * 4 * mr + 4);
+  D_.ensure(static_cast<size_t>(ncen) * M * mr + 4);
+  dD_.ensure(static_cast<size_t>(ncen) * M * mr + 4);
+  g_.ensure(static_cast<size_t>(ncen) * nmax * 3 + 3);
+  vir_.ensure(static_cast<size_t>(ncen) * 9 + 9);
+  e_.ensure(ncen + 1);
+  dp.X = X_.p;
+  dp.R = R_.p;
+  dp.Ad = Ad_.p;
+  dp.Bd = Bd_.p;
+  dp.D = D_.p;
+  dp.dD = dD_.p;
+  dp.g = g_.p;
+  dp.vir = vir_.p;
+  const int grid = std::max(1, std::min(ncen, 2 * n_sm_));
+  dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
+  scratch_.ensure(dp.scratch_slot * grid);
+  dp.scratch = scratch_.p;
+  tic("centre_forward");
+  launch_centre_forward(dp, grid, st_);
+  toc();
+  FitArgs fa{};
+  fa.n_fit = dp.n_fit;
+  int maxw = 0;
+  size_t ysum = 0;
+  for (int l = 0; l <= dp.n_fit; ++l) {
+    fa.fdims[l] = dp.fdims[l];
+    maxw = std::max(maxw, dp.fdims[l]);
+  }
+  for (int l = 0; l + 1 < dp.n_fit; ++l) ysum += static_cast<size_t>(dp.fdims[l + 1]);
+  fitY_.ensure(ysum * ncen + 4);
+  fitd_.ensure(2 * static_cast<size_t>(maxw) * ncen + 4);
+  {
+    size_t off = 0;
+    for (int l = 0; l + 1 < dp.n_fit; ++l) {
+      fa.Y[l] = fitY_.p + off;
+      off += static_cast<size_t>(dp.fdims[l + 1]) * ncen;
+    }
+  }
+  for (int l = 0; l < dp.n_fit; ++l) {
+    fa.fw[l] = dp.fw[l];
+    fa.fb[l] = dp.fb[l];
+  }
+  fa.n_centres = ncen;
+  fa.D = D_.p;
+  fa.delta[0] = fitd_.p;
+  fa.delta[1] = fitd_.p + static_cast<size_t>(maxw) * ncen;
+  fa.e = e_.p;
+  fa.dD = dD_.p;
+  tic("fit");
+  launch_fit(fa, st_);
+  toc();
+  tic("centre_backward");
+  launch_centre_backward(dp, grid, st_);
+  toc();
+  phases_.push_back({rank, 2, ph_in0, timers_.size() - 1});
+
+  // ---- forces --------------------------------------------------------------------------
+  const size_t ph_f0 = timers_.size();
+  fmem_.ensure(3 * static_cast<size_t>(nm) + 3);
+  ForceArgs fo{};
+  fo.nlist = nlist_.p;
+  fo.nn = nn_.p;
+  fo.n_max = nmax;
+  fo.cidx = cidx_.p;
+  fo.rlist = wide ? nullptr : rlist_.p;
+  fo.rn = wide ? nullptr : rn_.p;
+  fo.nloc = nloc;
+  fo.n_targets = wide ? nloc : nm;
+  fo.g = g_.p;
+  fo.fmem = fmem_.p;
+  tic("force_gather");
+  launch_force_gather(fo, st_);
+  toc();
+  AssembleArgs as{};
+  as.n_atoms = n;
+  as.rank = rank;
+  as.wide = wide;
+  as.owner = owner_.p;
+  as.loc_off = loc_off_.p;
+  as.gh_off = gh_off_.p;
+  as.counts = counts_.p;
+  as.fmem = fmem_.p;
+  as.e_centre = e_.p;
+  as.out = d_out;
+  tic("assemble");
+  launch_assemble(as, st_);
+  launch_energy_virial(e_.p, vir_.p, counts_.p, d_out, st_);
+  toc();
+  phases_.push_back({rank, 3, ph_f0, timers_.size() - 1});
+  if (!wide) {
+    CU(cudaMemcpyAsync(h_counts_ + 16 + (rank % 48), counts_.p + 3, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  }
+
+  if (keep_debug) {
+    CU(cudaStreamSynchronize(st_));
+    RankDebug& d = debug_[static_cast<size_t>(rank)];
+    std::vector<int> cm(ncen), mat(nm), msh(nm), mown(nm);
+    d.nn.assign(ncen, 0);
+    std::vector<int> nl(static_cast<size_t>(ncen) * nmax);
+    if (ncen) {
+      CU(cudaMemcpy(cm.data(), cen_member_.p, ncen * sizeof(int), cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(d.nn.data(), nn_.p, ncen * sizeof(int), cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(nl.data(), nlist_.p, nl.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    if (nm) {
+      CU(cudaMemcpy(mat.data(), m_atom_.p, nm * sizeof(int), cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(msh.data(), m_shift_.p, nm * sizeof(int), cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(mown.data(), m_owner_.p, nm * sizeof(int), cudaMemcpyDeviceToHost));
+    }
+    d.centre_atoms.resize(ncen);
+    d.nlist_atom.assign(static_cast<size_t>(ncen) * nmax, -1);
+    d.nlist_img.assign(static_cast<size_t>(ncen) * nmax * 3, 0);
+    for (int c = 0; c < ncen; ++c) {
+      const int mc = cm[c];
+      d.centre_atoms[c] = mat[mc];
+      const int cs = msh[mc];
+      for (int k = 0; k < std::min(d.nn[c], nmax); ++k) {
+        const int mj = nl[static_cast<size_t>(c) * nmax + k];
+        const int sj = msh[mj];
+        d.nlist_atom[static_cast<size_t>(c) * nmax + k] = mat[mj];
+        int* im = &d.nlist_img[(static_cast<size_t>(c) * nmax + k) * 3];
+        im[0] = shift_x_host(sj) - shift_x_host(cs);
+        im[1] = shift_y_host(sj) - shift_y_host(cs);
+        im[2] = shift_z_host(sj) - shift_z_host(cs);
+      }
+    }
+    d.ghost_atom.assign(mat.begin() + nloc, mat.end());
+    d.ghost_owner.assign(mown.begin() + nloc, mown.end());
+    d.ghost_shift.resize(static_cast<size_t>(ngh) * 3);
+    for (int gI = 0; gI < ngh; ++gI) {
+      const int s = msh[nloc + gI];
+      d.ghost_shift[3 * gI] = shift_x_host(s);
+      d.ghost_shift[3 * gI + 1] = shift_y_host(s);
+      d.ghost_shift[3 * gI + 2] = shift_z_host(s);
+    }
+  }
+}
+
+void Context::debug_rank(int rank, RankDebug& out) {
+  require(rank >= 0 && rank < opts_.n_ranks, "debug: bad rank");
+  require(keep_debug_, "debug: enable debug capture before compute");
+  out = debug_[static_cast<size_t>(rank)];
+}
+
+void Context::compute_host(long n, const double* pos, const int* types, const int64_t* gid,
+                           const double box[3], const uint8_t periodic[3], double* energy,
+                           double* forces, double* virial, double* atom_energy) {
+  for (long i = 0; i < n; ++i)
+    require(types[i] >= 0 && types[i] < model_.ns,
+            "dd_evaluate: species id outside the model's species table");
+  pos_.ensure(3 * static_cast<size_t>(n) + 3);
+  types_.ensure(static_cast<size_t>(n) + 1);
+  gid_.ensure(static_cast<size_t>(n) + 1);
+  out_.ensure(10 + 4 * static_cast<size_t>(n));
+  if (n) {
+    CU(cudaMemcpyAsync(pos_.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st_));
+    CU(cudaMemcpyAsync(types_.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st_));
+    if (gid) {
+      CU(cudaMemcpyAsync(gid_.p, gid, n * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+    } else {
+      std::vector<int64_t> iota(static_cast<size_t>(n));
+      for (long i = 0; i < n; ++i) iota[static_cast<size_t>(i)] = i;
+      CU(cudaMemcpyAsync(gid_.p, iota.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+      CU(cudaStreamSynchronize(st_));
+    }
+  }
+  compute_device(n, pos_.p, types_.p, gid_.p, box, periodic, out_.p);
+  double head[10];
+  CU(cudaMemcpyAsync(head, out_.p, sizeof head, cudaMemcpyDeviceToHost, st_));
+  if (n && forces) CU(cudaMemcpyAsync(forces, out_.p + 10, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (n && atom_energy)
+    CU(cudaMemcpyAsync(atom_energy, out_.p + 10 + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CU(cudaStreamSynchronize(st_));
+  if (energy) *energy = head[0];
+  if (virial) std::memcpy(virial, head + 1, 9 * sizeof(double));
+}
+
+}  // namespace nb

@@ -1,0 +1,116 @@
+// Device context: the B200 replacement of DpProvider + dd_evaluate.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "model.h"
+#include "nccl_dl.h"
+
+namespace nb {
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n);
+  void release();
+  ~DevBuf() { release(); }
+};
+
+struct RankStat {
+  long counts[4] = {0, 0, 0, 0};  // locals, ghosts, centres, route entries
+  double ms[4] = {0, 0, 0, 0};    // dd build, neighbour, inference, comm
+};
+
+struct RankDebug {  // parity hooks, filled on demand
+  std::vector<int> centre_atoms, nlist_atom, nlist_img, nn;
+  std::vector<int> ghost_atom, ghost_owner, ghost_shift;
+};
+
+struct Timer {
+  std::string name;
+  cudaEvent_t a, b;
+};
+
+class Context {
+ public:
+  Context(const Model& m, const nnmd_b200_opts& o);
+  ~Context();
+
+  // Full evaluation on device-resident inputs; result layout
+  // [E, W(9), F(3n), ae(n)] in d_out (float64).
+  void compute_device(long n, const double* d_pos, const int* d_types, const int64_t* d_gid,
+                      const double box[3], const uint8_t periodic[3], double* d_out);
+  void compute_host(long n, const double* pos, const int* types, const int64_t* gid,
+                    const double box[3], const uint8_t periodic[3], double* energy,
+                    double* forces, double* virial, double* atom_energy);
+
+  cudaStream_t stream() const { return st_; }
+  const RankStat& stat(int r) const { return stats_.at(static_cast<size_t>(r)); }
+  int n_ranks() const { return opts_.n_ranks; }
+  void debug_rank(int rank, RankDebug& out);
+  std::vector<std::pair<std::string, double>> kernel_times() const { return ktimes_; }
+
+ private:
+  void run_rank(int rank, const SysArgs& sys, const int dims[3], double thickness, double* d_out,
+                bool keep_debug);
+  void tic(const char* name);
+  void toc();
+  void collect_times();
+
+  Model model_;
+  DeviceWeightsHost wh_;
+  nnmd_b200_opts opts_;
+  cudaStream_t st_ = nullptr;
+  int n_sm_ = 148;
+  DevBuf<float> weights_;
+  NcclComm comm_ = nullptr;
+
+  // inputs (host-API path) and outputs
+  DevBuf<double> pos_, out_;
+  DevBuf<int> types_;
+  DevBuf<int64_t> gid_;
+  DevBuf<double> h_pinned_dummy_;
+  // step-global
+  DevBuf<int> owner_, err_;
+  // per rank (reused across virtual ranks)
+  DevBuf<int> is_local_, gcount_, loc_off_, gh_off_, counts_;
+  DevBuf<int> m_atom_, m_shift_, m_owner_, m_cell_, cflag_, coff_, cen_member_, cidx_;
+  DevBuf<double> m_pos_;
+  DevBuf<int> cell_count_, cell_start_, cell_fill_, cell_members_;
+  DevBuf<int> nlist_, nn_, rlist_, rn_;
+  DevBuf<float> X_, Ad_, Bd_, D_, dD_, scratch_, fitY_, fitd_;
+  DevBuf<float4> R_;
+  DevBuf<double> g_, vir_, e_, fmem_;
+  int* h_counts_ = nullptr;  // pinned
+  std::vector<RankStat> stats_;
+  std::vector<RankDebug> debug_;
+  std::vector<Timer> timers_;
+  std::vector<cudaEvent_t> pool_;
+  size_t pool_used_ = 0;
+  std::vector<std::pair<std::string, double>> ktimes_;
+  struct PhaseMark {
+    int rank;
+    int phase;
+    size_t t0, t1;  // timer indices
+  };
+  std::vector<PhaseMark> phases_;
+  int keep_debug_ = 0;
+  // pinned host staging for the host API
+  double* h_out_ = nullptr;
+  size_t h_out_cap_ = 0;
+
+ public:
+  void set_keep_debug(int v) { keep_debug_ = v; }
+};
+
+std::vector<int> partition_ranks(const double L[3], int n_ranks, double min_edge);
+
+}  // namespace nb
+
+struct nnmd_b200 {
+  nb::Context* ctx = nullptr;
+};

@@ -1,0 +1,467 @@
+// Domain-decomposition build, cell-list neighbour search and deterministic force
+// assembly (HBM/L2-bound integer + FP64 kernels).
+//
+// Reference algorithm: decomp.cpp:59-131 (ownership, halo), decomp.cpp:312-416 (members,
+// centres, per-centre scan, canonical sort, capacity), deeppot.cpp:141-148 (sort key),
+// deeppot.cpp:271-309 / decomp.cpp:421-538 (force assembly and ghost-force routing).
+#include <atomic>
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nb {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+
+// ----------------------------------------------------------------------------------
+// Ownership (owner_rank_of, decomp.cpp:59-68) + input validation
+// (neighbor.cpp:22-30 wrapped positions; deeppot.cpp:327-328 species range)
+// ----------------------------------------------------------------------------------
+__global__ void k_owner(SysArgs s, int dx, int dy, int dz, int* __restrict__ owner,
+                        int* __restrict__ err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.n) return;
+  const int dims[3] = {dx, dy, dz};
+  int c[3];
+  bool bad = s.species[i] < 0 || s.species[i] >= s.n_species;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double x = s.pos[3 * i + a];
+    if (s.per[a] && !(x >= 0.0 && x < s.L[a])) bad = true;
+    const double edge = s.L[a] / dims[a];
+    int k = static_cast<int>(floor(x / edge));
+    c[a] = min(max(k, 0), dims[a] - 1);
+  }
+  owner[i] = (c[0] * dims[1] + c[1]) * dims[2] + c[2];
+  if (bad) atomicMin(&err[0], i);
+}
+
+void launch_owner(const SysArgs& s, const int dims[3], int* owner, int* err, cudaStream_t st) {
+  if (s.n == 0) return;
+  k_owner<<<(s.n + 255) / 256, 256, 0, st>>>(s, dims[0], dims[1], dims[2], owner, err); count_launch();
+}
+
+// ----------------------------------------------------------------------------------
+// Halo slab test (build_halo, decomp.cpp:96-131): for every atom x 27 images,
+// q = p + k*L (FP64, no contraction) inside [slab_lo, slab_hi), own atoms excluded at
+// zero shift.  Pass 1 counts per atom; pass 2 writes members in (atom, shift) order.
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ bool in_slab(const double* q, const double* lo, const double* hi) {
+  return q[0] >= lo[0] && q[0] < hi[0] && q[1] >= lo[1] && q[1] < hi[1] && q[2] >= lo[2] &&
+         q[2] < hi[2];
+}
+
+__global__ void k_dd_flags(SysArgs s, RankArgs r, const int* __restrict__ owner,
+                           int* __restrict__ is_local, int* __restrict__ gcount) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.n) return;
+  const double p[3] = {s.pos[3 * i], s.pos[3 * i + 1], s.pos[3 * i + 2]};
+  const bool mine = owner[i] == r.rank;
+  int cnt = 0;
+  const int sx = s.per[0], sy = s.per[1], sz = s.per[2];
+  for (int kx = -sx; kx <= sx; ++kx)
+    for (int ky = -sy; ky <= sy; ++ky)
+      for (int kz = -sz; kz <= sz; ++kz) {
+        if (kx == 0 && ky == 0 && kz == 0 && mine) continue;
+        const double q[3] = {__dadd_rn(p[0], __dmul_rn(static_cast<double>(kx), s.L[0])),
+                             __dadd_rn(p[1], __dmul_rn(static_cast<double>(ky), s.L[1])),
+                             __dadd_rn(p[2], __dmul_rn(static_cast<double>(kz), s.L[2]))};
+        cnt += in_slab(q, r.slab_lo, r.slab_hi);
+      }
+  is_local[i] = mine;
+  gcount[i] = cnt;
+}
+
+void launch_dd_flags(const SysArgs& s, const RankArgs& r, const int* owner, int* is_local,
+                     int* gcount, cudaStream_t st) {
+  if (s.n == 0) return;
+  k_dd_flags<<<(s.n + 255) / 256, 256, 0, st>>>(s, r, owner, is_local, gcount); count_launch();
+}
+
+// Single-CTA exclusive scan (n up to a few 1e5; one launch, no host round trip).
+__global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ in, int* __restrict__ out,
+                                               int n) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? in[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int t = warp_tot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const int excl = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + x - v;
+    if (i < n) out[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[n] = carry;
+}
+
+void launch_scan(const int* in, int* out, int n, cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(in, out, n); count_launch();
+}
+
+// Members: locals first (ascending atom, shift 0), then ghosts in (atom, shift) order.
+__global__ void k_dd_members(SysArgs s, RankArgs r, const int* __restrict__ owner,
+                             const int* __restrict__ loc_off, const int* __restrict__ gh_off,
+                             int n_atoms, int* __restrict__ m_atom, int* __restrict__ m_shift,
+                             double* __restrict__ m_pos, int* __restrict__ m_owner) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= s.n) return;
+  const int nloc = loc_off[n_atoms];
+  const double p[3] = {s.pos[3 * i], s.pos[3 * i + 1], s.pos[3 * i + 2]};
+  const bool mine = owner[i] == r.rank;
+  if (mine) {
+    const int m = loc_off[i];
+    m_atom[m] = i;
+    m_shift[m] = kZeroShift;
+    m_owner[m] = r.rank;
+    for (int a = 0; a < 3; ++a) m_pos[3 * m + a] = p[a];
+  }
+  int m = nloc + gh_off[i];
+  const int sx = s.per[0], sy = s.per[1], sz = s.per[2];
+  for (int kx = -sx; kx <= sx; ++kx)
+    for (int ky = -sy; ky <= sy; ++ky)
+      for (int kz = -sz; kz <= sz; ++kz) {
+        if (kx == 0 && ky == 0 && kz == 0 && mine) continue;
+        const double q[3] = {__dadd_rn(p[0], __dmul_rn(static_cast<double>(kx), s.L[0])),
+                             __dadd_rn(p[1], __dmul_rn(static_cast<double>(ky), s.L[1])),
+                             __dadd_rn(p[2], __dmul_rn(static_cast<double>(kz), s.L[2]))};
+        if (!in_slab(q, r.slab_lo, r.slab_hi)) continue;
+        m_atom[m] = i;
+        m_shift[m] = pack_shift(kx, ky, kz);
+        m_owner[m] = owner[i];
+        for (int a = 0; a < 3; ++a) m_pos[3 * m + a] = q[a];
+        ++m;
+      }
+}
+
+void launch_dd_members(const SysArgs& s, const RankArgs& r, const int* owner, const int* loc_off,
+                       const int* gh_off, int n_atoms, int* m_atom, int* m_shift, double* m_pos,
+                       int* m_owner, cudaStream_t st) {
+  if (s.n == 0) return;
+  k_dd_members<<<(s.n + 255) / 256, 256, 0, st>>>(s, r, owner, loc_off, gh_off, n_atoms, m_atom,
+                                                  m_shift, m_pos, m_owner); count_launch();
+}
+
+// Centres: every local; for wide_halo also the first-layer ghosts (inside the rc slab,
+// decomp.cpp:317-326).
+__global__ void k_centre_flags(RankArgs r, const int* __restrict__ counts,
+                               const double* __restrict__ m_pos, int cap, int* __restrict__ flag) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nloc = counts[0], nm = counts[0] + counts[1];
+  if (m >= cap) return;
+  int f = 0;
+  if (m < nloc) f = 1;
+  else if (m < nm && r.wide) f = in_slab(m_pos + 3 * m, r.rc_lo, r.rc_hi);
+  flag[m] = f;
+}
+
+void launch_centre_flags(const RankArgs& r, const int* counts, const double* m_pos,
+                         int n_members_cap, int* flag, cudaStream_t st) {
+  if (n_members_cap == 0) return;
+  k_centre_flags<<<(n_members_cap + 255) / 256, 256, 0, st>>>(r, counts, m_pos, n_members_cap, flag); count_launch();
+}
+
+__global__ void k_centre_compact(const int* __restrict__ flag, const int* __restrict__ off,
+                                 int n, int* __restrict__ cen_member, int* __restrict__ cidx) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  if (flag[m]) {
+    cen_member[off[m]] = m;
+    cidx[m] = off[m];
+  } else {
+    cidx[m] = -1;
+  }
+}
+
+void launch_centre_compact(const int* flag, const int* off, int n_members, int* cen_member,
+                           int* cidx, cudaStream_t st) {
+  if (n_members == 0) return;
+  k_centre_compact<<<(n_members + 255) / 256, 256, 0, st>>>(flag, off, n_members, cen_member, cidx); count_launch();
+}
+
+// ----------------------------------------------------------------------------------
+// Cell grid over the materialised member images.  Width >= rc on every axis, so the
+// 27-cell stencil is complete; positions outside the grid clamp into the boundary
+// cells (adjacency preserved).  The grid only selects candidates: rows are then sorted
+// by the unique canonical key, so the result is independent of the grid geometry.
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ int cell_of(const CellArgs& c, const double* q) {
+  int id[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int k = static_cast<int>(floor((q[a] - c.origin[a]) / c.width[a]));
+    id[a] = min(max(k, 0), c.dims[a] - 1);
+  }
+  return (id[0] * c.dims[1] + id[1]) * c.dims[2] + id[2];
+}
+
+__global__ void k_cell_count(CellArgs c, const double* __restrict__ m_pos, int n,
+                             int* __restrict__ m_cell, int* __restrict__ count) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const int id = cell_of(c, m_pos + 3 * m);
+  m_cell[m] = id;
+  atomicAdd(&count[id], 1);
+}
+
+void launch_cell_count(const CellArgs& c, const double* m_pos, int n, int* m_cell, int* count,
+                       cudaStream_t st) {
+  if (n == 0) return;
+  k_cell_count<<<(n + 255) / 256, 256, 0, st>>>(c, m_pos, n, m_cell, count); count_launch();
+}
+
+__global__ void k_cell_fill(const int* __restrict__ m_cell, int n, const int* __restrict__ start,
+                            int* __restrict__ fill, int* __restrict__ members) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const int id = m_cell[m];
+  const int slot = atomicAdd(&fill[id], 1);
+  members[start[id] + slot] = m;
+}
+
+void launch_cell_fill(const int* m_cell, int n, const int* start, int* fill, int* members,
+                      cudaStream_t st) {
+  if (n == 0) return;
+  k_cell_fill<<<(n + 255) / 256, 256, 0, st>>>(m_cell, n, start, fill, members); count_launch();
+}
+
+// ----------------------------------------------------------------------------------
+// Neighbour rows: one warp per list owner (centre, or ghost target for reverse lists).
+// 27-cell stencil; candidate kept iff norm2(image_delta(...)) < rc^2 with the exact
+// FP64 expression of decomp.cpp:393-409 (rel shift = member shift - centre shift);
+// warp-ballot compaction into shared memory; canonical order (species, r^2, gid) by
+// rank sort (keys are unique); overflow (> n_max) recorded, never truncated.
+// ----------------------------------------------------------------------------------
+constexpr int kNbrWarps = 4;
+
+struct NbrEntry {
+  double r2;
+  int64_t gid;
+  int member;
+  int species;
+};
+
+__device__ __forceinline__ bool key_less(const NbrEntry& a, const NbrEntry& b) {
+  if (a.species != b.species) return a.species < b.species;
+  if (a.r2 != b.r2) return a.r2 < b.r2;
+  return a.gid < b.gid;
+}
+
+__global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap) {
+  extern __shared__ NbrEntry nbr_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  NbrEntry* buf = nbr_smem + static_cast<size_t>(wid) * cap;
+  const int li = blockIdx.x * kNbrWarps + wid;
+  if (li >= a.n_lists) return;
+  const int cm = a.centre_member ? a.centre_member[li] : li + a.member_offset;
+  const int ca = a.m_atom[cm];
+  const int cs = a.m_shift[cm];
+  const double pc[3] = {a.pos[3 * ca], a.pos[3 * ca + 1], a.pos[3 * ca + 2]};
+  const int csh[3] = {shift_x(cs), shift_y(cs), shift_z(cs)};
+  const int cell = a.m_cell[cm];
+  const int cz = cell % a.cdims[2], cy = (cell / a.cdims[2]) % a.cdims[1],
+            cx = cell / (a.cdims[1] * a.cdims[2]);
+  int cnt = 0;
+  for (int ox = -1; ox <= 1; ++ox) {
+    const int x = cx + ox;
+    if (x < 0 || x >= a.cdims[0]) continue;
+    for (int oy = -1; oy <= 1; ++oy) {
+      const int y = cy + oy;
+      if (y < 0 || y >= a.cdims[1]) continue;
+      for (int oz = -1; oz <= 1; ++oz) {
+        const int z = cz + oz;
+        if (z < 0 || z >= a.cdims[2]) continue;
+        const int id = (x * a.cdims[1] + y) * a.cdims[2] + z;
+        const int b = a.cell_start[id], e = a.cell_start[id + 1];
+        for (int base = b; base < e; base += 32) {
+          const int j = base + lane;
+          bool keep = false;
+          NbrEntry ent;
+          if (j < e) {
+            const int mj = a.cell_members[j];
+            if (mj != cm && mj < a.cand_limit) {
+              const int aj = a.m_atom[mj];
+              const int sj = a.m_shift[mj];
+              const int rel[3] = {shift_x(sj) - csh[0], shift_y(sj) - csh[1], shift_z(sj) - csh[2]};
+              const double dx = image_delta(a.pos[3 * aj], pc[0], rel[0], a.L[0]);
+              const double dy = image_delta(a.pos[3 * aj + 1], pc[1], rel[1], a.L[1]);
+              const double dz = image_delta(a.pos[3 * aj + 2], pc[2], rel[2], a.L[2]);
+              const double r2 = norm2_exact(dx, dy, dz);
+              if (r2 < a.rc2) {
+                keep = true;
+                ent.r2 = r2;
+                ent.gid = a.gid[aj];
+                ent.member = mj;
+                ent.species = a.species[aj];
+              }
+            }
+          }
+          const unsigned mask = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            const int slot = cnt + __popc(mask & ((1u << lane) - 1u));
+            if (slot < cap) buf[slot] = ent;
+          }
+          cnt += __popc(mask);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    a.nn[li] = cnt > a.n_max ? 0 : cnt;  // overflow: reported, list left empty
+    if (a.nonempty && cnt > 0) atomicAdd(a.nonempty, 1);
+  }
+  if (cnt > a.n_max) {
+    if (lane == 0) atomicMin(a.err, ca);
+    return;
+  }
+  int* out = a.nlist + static_cast<size_t>(li) * a.n_max;
+  for (int i = lane; i < cnt; i += 32) {
+    const NbrEntry me = buf[i];
+    int rank = 0;
+    for (int j = 0; j < cnt; ++j) rank += key_less(buf[j], me);
+    out[rank] = me.member;
+  }
+}
+
+void launch_neighbors(const NbrArgs& a, cudaStream_t st) {
+  if (a.n_lists == 0) return;
+  const int cap = ((a.n_max + 1 + 31) / 32) * 32;
+  const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_neighbors, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  k_neighbors<<<(a.n_lists + kNbrWarps - 1) / kNbrWarps, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
+}
+
+// ----------------------------------------------------------------------------------
+// prod_force as a deterministic warp-segmented gather (no floating-point atomics).
+// Target member t receives  +sum_k g[own centre][k]   (its centre self-term,
+// center_grad = -sum g, F = -partials; deeppot.cpp:256-262, 300-309)
+// and -g[c][k] for every row (c, k) of another centre c that lands on t.  Incoming
+// centres are enumerated from t's own list (locals) or its reverse list (ghosts), the
+// row k by a coalesced warp scan of c's member list.  Fixed summation order.
+// ----------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_force_gather(ForceArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= a.n_targets) return;
+  double own[3] = {0, 0, 0};
+  const int oc = a.cidx[t];
+  if (oc >= 0) {
+    const int n = a.nn[oc];
+    const double* g = a.g + static_cast<size_t>(oc) * a.n_max * 3;
+    for (int k = lane; k < n; k += 32)
+      for (int c = 0; c < 3; ++c) own[c] += g[3 * k + c];
+    for (int c = 0; c < 3; ++c) own[c] = warp_sum(own[c]);
+  }
+  const int* list;
+  int cnt;
+  if (t < a.nloc) {
+    list = a.nlist + static_cast<size_t>(oc) * a.n_max;
+    cnt = a.nn[oc];
+  } else {
+    list = a.rlist + static_cast<size_t>(t - a.nloc) * a.n_max;
+    cnt = a.rn[t - a.nloc];
+  }
+  double in[3] = {0, 0, 0};
+  for (int e = 0; e < cnt; ++e) {
+    const int c = a.cidx[list[e]];
+    if (c < 0) continue;
+    const int nc = a.nn[c];
+    const int* row = a.nlist + static_cast<size_t>(c) * a.n_max;
+    int k = -1;
+    for (int base = 0; base < nc && k < 0; base += 32) {
+      const int j = base + lane;
+      const unsigned hit = __ballot_sync(0xffffffffu, j < nc && row[j] == t);
+      if (hit) k = base + __ffs(hit) - 1;
+    }
+    if (k >= 0) {
+      const double* g = a.g + (static_cast<size_t>(c) * a.n_max + k) * 3;
+      for (int q = 0; q < 3; ++q) in[q] += g[q];
+    }
+  }
+  if (lane == 0)
+    for (int q = 0; q < 3; ++q) a.fmem[3 * static_cast<size_t>(t) + q] = own[q] - in[q];
+}
+
+void launch_force_gather(const ForceArgs& a, cudaStream_t st) {
+  if (a.n_targets == 0) return;
+  const long threads = static_cast<long>(a.n_targets) * 32;
+  k_force_gather<<<static_cast<int>((threads + 127) / 128), 128, 0, st>>>(a); count_launch();
+}
+
+// Per-atom assembly: owner's zero-image partial first, then the ghost images of the atom
+// in shift order (the masked route, decomp.cpp:502-536); wide_halo keeps locals only.
+// Accumulates into the step output (virtual ranks run in ascending order).
+__global__ void k_assemble(AssembleArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n_atoms) return;
+  const int nloc = a.counts[0];
+  double f[3] = {0, 0, 0};
+  const bool mine = a.owner[i] == a.rank;
+  if (mine) {
+    const int m = a.loc_off[i];
+    for (int c = 0; c < 3; ++c) f[c] += a.fmem[3 * static_cast<size_t>(m) + c];
+    a.out[10 + 3 * static_cast<size_t>(a.n_atoms) + i] = a.e_centre[m];
+  }
+  if (!a.wide)
+    for (int m = nloc + a.gh_off[i]; m < nloc + a.gh_off[i + 1]; ++m)
+      for (int c = 0; c < 3; ++c) f[c] += a.fmem[3 * static_cast<size_t>(m) + c];
+  for (int c = 0; c < 3; ++c) a.out[10 + 3 * static_cast<size_t>(i) + c] += f[c];
+}
+
+void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
+  if (a.n_atoms == 0) return;
+  k_assemble<<<(a.n_atoms + 255) / 256, 256, 0, st>>>(a); count_launch();
+}
+
+__global__ void __launch_bounds__(256) k_energy_virial(const double* __restrict__ e,
+                                                       const double* __restrict__ vir,
+                                                       const int* __restrict__ counts,
+                                                       double* __restrict__ out) {
+  __shared__ double red[8];
+  const int nloc = counts[0];
+  double acc[10] = {0};
+  for (int c = threadIdx.x; c < nloc; c += blockDim.x) {
+    acc[0] += e[c];
+    for (int q = 0; q < 9; ++q) acc[1 + q] += vir[9 * static_cast<size_t>(c) + q];
+  }
+  for (int q = 0; q < 10; ++q) {
+    const double t = block_sum(acc[q], red);
+    if (threadIdx.x == 0) out[q] += t;
+  }
+}
+
+void launch_energy_virial(const double* e, const double* vir, const int* counts, double* out,
+                          cudaStream_t st) {
+  k_energy_virial<<<1, 256, 0, st>>>(e, vir, counts, out); count_launch();
+}
+
+}  // namespace nb

@@ -1,0 +1,611 @@
+// DPA-1 network kernels: per-centre fused forward / exact backward and the batched
+// fitting net.  FP32 arithmetic (FP64 geometry), one CTA per centre in a persistent
+// grid; per-centre matrices live in an L2-resident per-CTA scratch slot.
+//
+// Reference semantics (dp_core.hpp):
+//   rows / switch / env           200-223, 116-137
+//   embedding (tanh every layer)  235-250
+//   gated attention x n_attn      252-356   (weighted softmax 300-329, gate 280-296)
+//   descriptor                    358-384
+//   fitting net                   386-391
+//   exact backward                396-614   (row gradients 597-611)
+//
+// Attention is evaluated in the re-associated form (see model.cpp fold_weights):
+//   U = X [A | B]   (A = Wq Wk^T / sqrt(d_a), B = Wv Wo),  S = U_A X^T,
+//   P~ = (s_j^2 pu) o Theta,  X' = X + P~ U_B
+// and its exact reverse:
+//   dP~ = dY U_B^T, dU_B = P~^T dY, dS = P o (dP - t), dU_A = dS X,
+//   dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T
+#include <cfloat>
+
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "kernels.h"
+
+namespace nb {
+
+namespace {
+
+struct Slot {
+  float *U, *PU, *PT, *T, *Qb, *DX0, *DX1, *dU, *EMB;
+};
+
+__host__ __device__ inline int max_width(const DpArgs& a) {
+  int w = a.M;
+  for (int e = 0; e < a.n_embed; ++e) w = w > a.edims[e] ? w : a.edims[e];
+  return w;
+}
+
+__host__ __device__ inline size_t emb_floats(const DpArgs& a) {
+  size_t t = 0;
+  for (int e = 0; e + 1 < a.n_embed; ++e) t += static_cast<size_t>(a.n_max) * a.edims[e];
+  return t;
+}
+
+__host__ __device__ inline size_t align4(size_t x) { return (x + 3) & ~size_t(3); }
+
+__device__ inline Slot slot_of(const DpArgs& a, float* base) {
+  const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a);
+  Slot s;
+  size_t o = 0;
+  s.U = base + o;   o += align4(nm * M2);
+  s.PU = base + o;  o += align4(nm * nm);
+  s.PT = base + o;  o += align4(nm * nm);
+  s.T = base + o;   o += align4(nm * nm);
+  s.Qb = base + o;  o += align4(nm * nm);
+  s.DX0 = base + o; o += align4(nm * W);
+  s.DX1 = base + o; o += align4(nm * W);
+  s.dU = base + o;  o += align4(nm * M2);
+  s.EMB = base + o;
+  return s;
+}
+
+struct Smem {
+  GemmSmem* gs;
+  float4* R;
+  float4* dR;
+  float* s;
+  float* dsx;
+  float* t;
+  float* rowpart;
+  float* Ad;
+  float* Bd;
+  float* dAd;
+  float* dBd;
+  int* z;
+  double* red;
+};
+
+__host__ __device__ inline size_t smem_layout(const DpArgs& a, unsigned char* base, Smem* out) {
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    o = (o + 15) & ~size_t(15);
+    unsigned char* p = base ? base + o : nullptr;
+    o += bytes;
+    return p;
+  };
+  Smem s;
+  s.gs = reinterpret_cast<GemmSmem*>(take(sizeof(GemmSmem)));
+  s.R = reinterpret_cast<float4*>(take(sizeof(float4) * a.n_max));
+  s.dR = reinterpret_cast<float4*>(take(sizeof(float4) * a.n_max));
+  s.s = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
+  s.dsx = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
+  s.t = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
+  s.rowpart = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
+  s.Ad = reinterpret_cast<float*>(take(sizeof(float) * a.M * 4));
+  s.Bd = reinterpret_cast<float*>(take(sizeof(float) * 4 * a.mr));
+  s.dAd = reinterpret_cast<float*>(take(sizeof(float) * a.M * 4));
+  s.dBd = reinterpret_cast<float*>(take(sizeof(float) * 4 * a.mr));
+  s.z = reinterpret_cast<int*>(take(sizeof(int) * a.n_max));
+  s.red = reinterpret_cast<double*>(take(sizeof(double) * 32));
+  if (out) *out = s;
+  return o;
+}
+
+__device__ __forceinline__ float dot4(const float4& a, const float4& b) {
+  return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
+}
+
+// Row geometry of centre c: r, s (FP64), env row R = (s, s/r d) -> float.  Returns sigma.
+__device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int& zi) {
+  const int cm = a.cen_member[c];
+  const int ca = a.m_atom[cm];
+  const int cs = a.m_shift[cm];
+  zi = a.species[ca];
+  const int* list = a.nlist + static_cast<size_t>(c) * a.n_max;
+  double sig = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int mj = list[k];
+    const int aj = a.m_atom[mj];
+    const int sj = a.m_shift[mj];
+    const int rel[3] = {shift_x(sj) - shift_x(cs), shift_y(sj) - shift_y(cs), shift_z(sj) - shift_z(cs)};
+    double d[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) d[q] = image_delta(a.pos[3 * aj + q], a.pos[3 * ca + q], rel[q], a.L[q]);
+    const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
+    double s, ds;
+    switch_fn(r, a.rcs, a.rc, s, ds);
+    const double sr = s / r;
+    const float4 R = make_float4(static_cast<float>(s), static_cast<float>(sr * d[0]),
+                                 static_cast<float>(sr * d[1]), static_cast<float>(sr * d[2]));
+    sm.R[k] = R;
+    sm.s[k] = static_cast<float>(s);
+    sm.z[k] = a.species[aj];
+    sig += s * s;
+  }
+  return block_sum(sig, sm.red);
+}
+
+// Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
+// Writes intermediate activations to EMB and the last to `out` (n x M).
+__device__ void embed_forward(const DpArgs& a, int n, int zi, const Smem& sm, const Slot& sl,
+                              float* out) {
+  const int E0 = a.edims[0];
+  float* cur = (a.n_embed == 1) ? out : sl.EMB;
+  for (int idx = threadIdx.x; idx < n * E0; idx += blockDim.x) {
+    const int k = idx / E0, o = idx - k * E0;
+    const float v = fmaf(sm.s[k], a.w0[o], a.ctab[(static_cast<size_t>(sm.z[k]) * a.ns + zi) * E0 + o]);
+    cur[idx] = tanhf(v);
+  }
+  __syncthreads();
+  size_t off = static_cast<size_t>(a.n_max) * E0;
+  for (int e = 1; e < a.n_embed; ++e) {
+    const int Ein = a.edims[e - 1], Eout = a.edims[e];
+    float* nxt = (e + 1 == a.n_embed) ? out : sl.EMB + off;
+    const float* b = a.eb[e];
+    bgemm<false, true>(n, Eout, Ein, cur, Ein, a.ew[e], Ein, *sm.gs,
+                       [&](int m, int o, float v) { nxt[m * Eout + o] = tanhf(v + b[o]); });
+    __syncthreads();
+    cur = nxt;
+    off += static_cast<size_t>(a.n_max) * Eout;
+  }
+}
+
+// Weighted softmax + gate for every row: PU = pu (optional), PT = s_j^2 pu Theta.
+__device__ void softmax_gate(int n, const float* S, float* PU, float* PT, float inv_sig,
+                             const Smem& sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = wid; k < n; k += nw) {
+    const float* row = S + static_cast<size_t>(k) * n;
+    float mx = -FLT_MAX;
+    for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
+    mx = warp_max(mx);
+    float den = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float sj = sm.s[j];
+      den += sj * sj * expf(row[j] - mx);
+    }
+    den = warp_sum(den);
+    const float inv = den > 0.f ? 1.0f / den : 0.f;
+    const float4 Rk = sm.R[k];
+    for (int j = lane; j < n; j += 32) {
+      const float sj = sm.s[j];
+      const float pu = expf(row[j] - mx) * inv;
+      const float th = dot4(Rk, sm.R[j]) * inv_sig;
+      if (PU) PU[static_cast<size_t>(k) * n + j] = pu;
+      PT[static_cast<size_t>(k) * n + j] = sj * sj * pu * th;
+    }
+  }
+}
+
+}  // namespace
+
+size_t dp_scratch_floats(const DpArgs& a) {
+  const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a);
+  return align4(nm * M2) * 2 + align4(nm * nm) * 4 + align4(nm * W) * 2 + emb_floats(a) + 64;
+}
+
+size_t dp_smem_bytes(const DpArgs& a) { return smem_layout(a, nullptr, nullptr) + 16; }
+
+// ------------------------------------------------------------------------------------
+// Forward: rows -> embedding -> attention layers -> descriptor D = (X^T R)(R^T X_<) / n_max
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_centre_forward(const __grid_constant__ DpArgs a) {
+  extern __shared__ __align__(16) unsigned char dp_smem[];
+  Smem sm;
+  smem_layout(a, dp_smem, &sm);
+  const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
+  const int M = a.M, M2 = 2 * M, mr = a.mr;
+  for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
+    const int n = a.nn[c];
+    int zi;
+    const double sig = centre_rows(a, c, n, sm, zi);
+    const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
+    float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) Rg[k] = sm.R[k];
+    float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
+    embed_forward(a, n, zi, sm, sl, X);
+    for (int l = 0; l < a.n_attn; ++l) {
+      const float* Xl = X + l * a.x_layer_stride;
+      float* Xn = X + (l + 1) * a.x_layer_stride;
+      bgemm<false, false>(n, M2, M, Xl, M, a.ab[l], M2, *sm.gs,
+                          [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
+      __syncthreads();
+      bgemm<false, true>(n, n, M, sl.U, M2, Xl, M, *sm.gs,
+                         [&](int k, int j, float v) { sl.PU[k * n + j] = v; });
+      __syncthreads();
+      softmax_gate(n, sl.PU, nullptr, sl.PT, inv_sig, sm);
+      __syncthreads();
+      bgemm<false, false>(n, M, n, sl.PT, n, sl.U + M, M2, *sm.gs,
+                          [&](int k, int m, float v) { Xn[k * M + m] = Xl[k * M + m] + v; });
+      __syncthreads();
+    }
+    // descriptor (dp_core.hpp:358-384)
+    const float* Xf = X + a.n_attn * a.x_layer_stride;
+    for (int idx = threadIdx.x; idx < M * 4 + 4 * mr; idx += blockDim.x) {
+      float acc = 0.f;
+      if (idx < M * 4) {
+        const int m = idx >> 2, q = idx & 3;
+        for (int k = 0; k < n; ++k) acc += Xf[k * M + m] * reinterpret_cast<const float*>(&sm.R[k])[q];
+        sm.Ad[idx] = acc * a.inv_sqrt_nmax;
+      } else {
+        const int j = idx - M * 4, q = j / mr, r = j - q * mr;
+        for (int k = 0; k < n; ++k) acc += reinterpret_cast<const float*>(&sm.R[k])[q] * Xf[k * M + r];
+        sm.Bd[j] = acc * a.inv_sqrt_nmax;
+      }
+    }
+    __syncthreads();
+    float* D = a.D + static_cast<size_t>(c) * M * mr;
+    for (int idx = threadIdx.x; idx < M * mr; idx += blockDim.x) {
+      const int m = idx / mr, q = idx - m * mr;
+      float acc = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) acc += sm.Ad[m * 4 + cc] * sm.Bd[cc * mr + q];
+      D[idx] = acc;
+    }
+    for (int idx = threadIdx.x; idx < M * 4; idx += blockDim.x) a.Ad[static_cast<size_t>(c) * M * 4 + idx] = sm.Ad[idx];
+    for (int idx = threadIdx.x; idx < 4 * mr; idx += blockDim.x) a.Bd[static_cast<size_t>(c) * 4 * mr + idx] = sm.Bd[idx];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Backward: dD -> (dA, dB) -> dX, dR -> attention layers in reverse -> embedding ->
+// row gradients g_k = de/dd_k (FP64 geometry), per-centre virial -sum g (x) d.
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_centre_backward(const __grid_constant__ DpArgs a) {
+  extern __shared__ __align__(16) unsigned char dp_smem[];
+  Smem sm;
+  smem_layout(a, dp_smem, &sm);
+  const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
+  const int M = a.M, M2 = 2 * M, mr = a.mr;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
+    const int n = a.nn[c];
+    int zi;
+    const double sig = centre_rows(a, c, n, sm, zi);
+    const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
+    const float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
+    const float* Xf = X + a.n_attn * a.x_layer_stride;
+    const float* dD = a.dD + static_cast<size_t>(c) * M * mr;
+    const float* Ad = a.Ad + static_cast<size_t>(c) * M * 4;
+    const float* Bd = a.Bd + static_cast<size_t>(c) * 4 * mr;
+    // dA[m][cc] = sum_q dD[m,q] B[cc,q];  dB[cc][q] = sum_m dD[m,q] A[m,cc]
+    for (int idx = threadIdx.x; idx < M * 4 + 4 * mr; idx += blockDim.x) {
+      float acc = 0.f;
+      if (idx < M * 4) {
+        const int m = idx >> 2, cc = idx & 3;
+        for (int q = 0; q < mr; ++q) acc += dD[m * mr + q] * Bd[cc * mr + q];
+        sm.dAd[idx] = acc;
+      } else {
+        const int j = idx - M * 4, cc = j / mr, q = j - cc * mr;
+        for (int m = 0; m < M; ++m) acc += dD[m * mr + q] * Ad[m * 4 + cc];
+        sm.dBd[j] = acc;
+      }
+    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) sm.dsx[k] = 0.f;
+    __syncthreads();
+    float* dY = sl.DX0;
+    float* dXn = sl.DX1;
+    const float inm = a.inv_sqrt_nmax;
+    for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
+      const int k = idx / M, m = idx - k * M;
+      const float* R = reinterpret_cast<const float*>(&sm.R[k]);
+      float v = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) v += sm.dAd[m * 4 + cc] * R[cc];
+      if (m < mr)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) v += sm.dBd[cc * mr + m] * R[cc];
+      dY[idx] = v * inm;
+    }
+    for (int idx = threadIdx.x; idx < n * 4; idx += blockDim.x) {
+      const int k = idx >> 2, cc = idx & 3;
+      float v = 0.f;
+      for (int m = 0; m < M; ++m) v += Xf[k * M + m] * sm.dAd[m * 4 + cc];
+      for (int q = 0; q < mr; ++q) v += Xf[k * M + q] * sm.dBd[cc * mr + q];
+      reinterpret_cast<float*>(&sm.dR[k])[cc] = v * inm;
+    }
+    __syncthreads();
+    for (int l = a.n_attn - 1; l >= 0; --l) {
+      const float* Xl = X + l * a.x_layer_stride;
+      const float* AB = a.ab[l];
+      bgemm<false, false>(n, M2, M, Xl, M, AB, M2, *sm.gs,
+                          [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
+      __syncthreads();
+      bgemm<false, true>(n, n, M, sl.U, M2, Xl, M, *sm.gs,
+                         [&](int k, int j, float v) { sl.PU[k * n + j] = v; });
+      __syncthreads();
+      softmax_gate(n, sl.PU, sl.PU, sl.PT, inv_sig, sm);
+      __syncthreads();
+      // T = dP~ = dY U_B^T
+      bgemm<false, true>(n, n, M, dY, M, sl.U + M, M2, *sm.gs,
+                         [&](int k, int j, float v) { sl.T[k * n + j] = v; });
+      __syncthreads();
+      // row pass: dP = dP~ Theta, dC = dP~ P / sigma, t_k, dsigma partials
+      for (int k = wid; k < n; k += nw) {
+        const float4 Rk = sm.R[k];
+        float t = 0.f, dsg = 0.f;
+        for (int j = lane; j < n; j += 32) {
+          const size_t kj = static_cast<size_t>(k) * n + j;
+          const float sj = sm.s[j];
+          const float C = dot4(Rk, sm.R[j]);
+          const float dpt = sl.T[kj];
+          const float pv = sj * sj * sl.PU[kj];
+          const float dP = dpt * C * inv_sig;
+          sl.T[kj] = dP;
+          sl.Qb[kj] = dpt * pv * inv_sig;
+          dsg -= dpt * pv * C * inv_sig * inv_sig;
+          t += dP * pv;
+        }
+        t = warp_sum(t);
+        dsg = warp_sum(dsg);
+        if (lane == 0) {
+          sm.t[k] = t;
+          sm.rowpart[k] = dsg;
+        }
+      }
+      __syncthreads();
+      // column pass: dw_j (softmax weights s_j^2) and the gate's dR_j
+      for (int j = wid; j < n; j += nw) {
+        float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+        for (int k = lane; k < n; k += 32) {
+          const size_t kj = static_cast<size_t>(k) * n + j;
+          dw += sl.PU[kj] * (sl.T[kj] - sm.t[k]);
+          const float sym = sl.Qb[kj] + sl.Qb[static_cast<size_t>(j) * n + k];
+          const float4 Rk = sm.R[k];
+          g0 += sym * Rk.x;
+          g1 += sym * Rk.y;
+          g2 += sym * Rk.z;
+          g3 += sym * Rk.w;
+        }
+        dw = warp_sum(dw);
+        g0 = warp_sum(g0);
+        g1 = warp_sum(g1);
+        g2 = warp_sum(g2);
+        g3 = warp_sum(g3);
+        if (lane == 0) {
+          sm.dsx[j] += 2.f * sm.s[j] * dw;
+          float4 r = sm.dR[j];
+          r.x += g0;
+          r.y += g1;
+          r.z += g2;
+          r.w += g3;
+          sm.dR[j] = r;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float ds = 0.f;
+        for (int k = 0; k < n; ++k) ds += sm.rowpart[k];
+        sm.red[0] = ds;
+      }
+      __syncthreads();
+      const float dsig = static_cast<float>(sm.red[0]);
+      for (int k = threadIdx.x; k < n; k += blockDim.x) sm.dsx[k] += 2.f * sm.s[k] * dsig;
+      // dS = P o (dP - t)
+      for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+        const int k = idx / n, j = idx - k * n;
+        const float sj = sm.s[j];
+        sl.T[idx] = sj * sj * sl.PU[idx] * (sl.T[idx] - sm.t[k]);
+      }
+      __syncthreads();
+      // dU_A = dS X ; dU_B = P~^T dY
+      bgemm<false, false>(n, M, n, sl.T, n, Xl, M, *sm.gs,
+                          [&](int k, int m, float v) { sl.dU[k * M2 + m] = v; });
+      bgemm<true, false>(n, M, n, sl.PT, n, dY, M, *sm.gs,
+                         [&](int k, int m, float v) { sl.dU[k * M2 + M + m] = v; });
+      __syncthreads();
+      // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T
+      bgemm<true, false>(n, M, n, sl.T, n, sl.U, M2, *sm.gs,
+                         [&](int k, int m, float v) { dXn[k * M + m] = dY[k * M + m] + v; });
+      __syncthreads();
+      bgemm<false, true>(n, M, M2, sl.dU, M2, AB, M2, *sm.gs,
+                         [&](int k, int m, float v) { dXn[k * M + m] += v; });
+      __syncthreads();
+      float* tmp = dY;
+      dY = dXn;
+      dXn = tmp;
+    }
+    // embedding backward (dp_core.hpp:580-596): recompute hidden activations
+    if (a.n_embed > 1) {
+      embed_forward(a, n, zi, sm, sl, dXn);  // last layer output discarded (== X_0)
+    }
+    const float* X0 = X;
+    for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
+      const float y = X0[idx];
+      dY[idx] *= 1.f - y * y;
+    }
+    __syncthreads();
+    {
+      // offsets of the stored activations
+      size_t offs[kMaxLayers];
+      size_t off = 0;
+      for (int e = 0; e + 1 < a.n_embed; ++e) {
+        offs[e] = off;
+        off += static_cast<size_t>(a.n_max) * a.edims[e];
+      }
+      for (int e = a.n_embed - 1; e >= 1; --e) {
+        const int Ein = a.edims[e - 1], Eout = a.edims[e];
+        const float* h = sl.EMB + offs[e - 1];
+        bgemm<false, false>(n, Ein, Eout, dY, Eout, a.ew[e], Ein, *sm.gs,
+                            [&](int k, int i, float v) {
+                              const float y = h[k * Ein + i];
+                              dXn[k * Ein + i] = v * (1.f - y * y);
+                            });
+        __syncthreads();
+        float* tmp = dY;
+        dY = dXn;
+        dXn = tmp;
+      }
+      const int E0 = a.edims[0];
+      for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        float du = 0.f;
+        for (int o = 0; o < E0; ++o) du += dY[k * E0 + o] * a.w0[o];
+        sm.dsx[k] += du;
+      }
+      __syncthreads();
+    }
+    // row gradients (dp_core.hpp:597-611) in FP64 geometry; virial W_ab -= g_a d_b
+    {
+      const int cm = a.cen_member[c];
+      const int ca = a.m_atom[cm];
+      const int cs = a.m_shift[cm];
+      const int* list = a.nlist + static_cast<size_t>(c) * a.n_max;
+      double* g = a.g + static_cast<size_t>(c) * a.n_max * 3;
+      double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int mj = list[k];
+        const int aj = a.m_atom[mj];
+        const int sj = a.m_shift[mj];
+        const int rel[3] = {shift_x(sj) - shift_x(cs), shift_y(sj) - shift_y(cs), shift_z(sj) - shift_z(cs)};
+        double d[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) d[q] = image_delta(a.pos[3 * aj + q], a.pos[3 * ca + q], rel[q], a.L[q]);
+        const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
+        double s, ds;
+        switch_fn(r, a.rcs, a.rc, s, ds);
+        const double ir = 1.0 / r, sr = s * ir;
+        const double e[3] = {d[0] * ir, d[1] * ir, d[2] * ir};
+        const float4 dr = sm.dR[k];
+        const double dr0 = dr.x, dr1 = dr.y, dr2 = dr.z, dr3 = dr.w;
+        const double ge = dr1 * e[0] + dr2 * e[1] + dr3 * e[2];
+        const double coef = (dr0 + static_cast<double>(sm.dsx[k])) * ds + (ds - sr) * ge;
+        const double gk[3] = {coef * e[0] + sr * dr1, coef * e[1] + sr * dr2, coef * e[2] + sr * dr3};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          g[3 * k + q] = gk[q];
+#pragma unroll
+          for (int b = 0; b < 3; ++b) w[3 * q + b] -= gk[q] * d[b];
+        }
+      }
+      for (int q = 0; q < 9; ++q) {
+        const double t = block_sum(w[q], sm.red + 8);
+        if (threadIdx.x == 0) a.vir[static_cast<size_t>(c) * 9 + q] = t;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st) {
+  if (a.n_centres == 0) return;
+  const size_t smem = dp_smem_bytes(a);
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_centre_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_centre_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set = smem;
+  }
+  k_centre_forward<<<grid, 256, smem, st>>>(a); count_launch();
+}
+
+void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st) {
+  if (a.n_centres == 0) return;
+  const size_t smem = dp_smem_bytes(a);
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_centre_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_centre_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set = smem;
+  }
+  k_centre_backward<<<grid, 256, smem, st>>>(a); count_launch();
+}
+
+// ------------------------------------------------------------------------------------
+// Fitting net over all centres (dp_core.hpp:386-391 forward; 408-414 backward)
+// ------------------------------------------------------------------------------------
+enum { EPI_STORE = 0, EPI_TANH_BIAS = 1, EPI_DTANH = 2 };
+
+template <bool TB>
+__global__ void __launch_bounds__(256) k_fit_gemm(int M, int N, int K, const float* __restrict__ A,
+                                                  const float* __restrict__ B, int ldb,
+                                                  float* __restrict__ C, const float* __restrict__ bias,
+                                                  const float* __restrict__ Y, int mode) {
+  __shared__ GemmSmem gs;
+  const int m0 = blockIdx.y * kTM, n0 = blockIdx.x * kTN;
+  const int Ms = min(kTM, M - m0), Ns = min(kTN, N - n0);
+  const float* Ab = A + static_cast<size_t>(m0) * K;
+  const float* Bb = TB ? B + static_cast<size_t>(n0) * ldb : B + n0;
+  bgemm<false, TB>(Ms, Ns, K, Ab, K, Bb, ldb, gs, [&](int m, int n, float v) {
+    const size_t o = static_cast<size_t>(m0 + m) * N + n0 + n;
+    if (mode == EPI_TANH_BIAS) v = tanhf(v + bias[n0 + n]);
+    else if (mode == EPI_DTANH) {
+      const float y = Y[o];
+      v *= 1.f - y * y;
+    }
+    C[o] = v;
+  });
+}
+
+// e[c] = b + w . Y[c]   (linear output layer); delta[c][o] = w[o] (1 - Y[c][o]^2)
+__global__ void k_fit_out(int nc, int H, const float* __restrict__ Y, const float* __restrict__ w,
+                          const float* __restrict__ b, double* __restrict__ e, float* __restrict__ delta) {
+  const int lane = threadIdx.x & 31;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= nc) return;
+  const float* y = Y + static_cast<size_t>(c) * H;
+  float acc = 0.f;
+  for (int o = lane; o < H; o += 32) {
+    const float v = y[o];
+    acc += w[o] * v;
+    if (delta) delta[static_cast<size_t>(c) * H + o] = w[o] * (1.f - v * v);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) e[c] = static_cast<double>(acc) + static_cast<double>(b[0]);
+}
+
+__global__ void k_fill_rows(int nc, int H, const float* __restrict__ w, float* __restrict__ out) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<size_t>(nc) * H) return;
+  out[i] = w[i % H];
+}
+
+void launch_fit(const FitArgs& a, cudaStream_t st) {
+  const int nc = a.n_centres;
+  if (nc == 0) return;
+  const int L = a.n_fit;
+  auto gemm = [&](bool tb, int N, int K, const float* A, const float* B, int ldb, float* C,
+                  const float* bias, const float* Y, int mode) {
+    dim3 grid((N + kTN - 1) / kTN, (nc + kTM - 1) / kTM);
+    if (tb) k_fit_gemm<true><<<grid, 256, 0, st>>>(nc, N, K, A, B, ldb, C, bias, Y, mode);
+    else k_fit_gemm<false><<<grid, 256, 0, st>>>(nc, N, K, A, B, ldb, C, bias, Y, mode);
+    count_launch();
+  };
+  // forward hidden layers: Y_l = tanh(X W_l^T + b_l)
+  const float* x = a.D;
+  for (int l = 0; l + 1 < L; ++l) {
+    gemm(true, a.fdims[l + 1], a.fdims[l], x, a.fw[l], a.fdims[l], a.Y[l], a.fb[l], nullptr, EPI_TANH_BIAS);
+    x = a.Y[l];
+  }
+  const int H = a.fdims[L - 1];
+  if (L == 1) {
+    // e = b + w . D ; dD = w
+    k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, H, a.D, a.fw[0], a.fb[0], a.e, nullptr); count_launch();
+    k_fill_rows<<<static_cast<int>((static_cast<size_t>(nc) * H + 255) / 256), 256, 0, st>>>(nc, H, a.fw[0], a.dD); count_launch();
+    return;
+  }
+  float* dcur = a.delta[0];
+  float* dnxt = a.delta[1];
+  k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, H, a.Y[L - 2], a.fw[L - 1], a.fb[L - 1], a.e, dcur); count_launch();
+  // delta_{l-1} = (delta_l W_l) o (1 - Y_{l-1}^2);  dD = delta_0 W_0
+  for (int l = L - 2; l >= 1; --l) {
+    gemm(false, a.fdims[l], a.fdims[l + 1], dcur, a.fw[l], a.fdims[l], dnxt, nullptr, a.Y[l - 1], EPI_DTANH);
+    float* t = dcur;
+    dcur = dnxt;
+    dnxt = t;
+  }
+  gemm(false, a.fdims[0], a.fdims[1], dcur, a.fw[0], a.fdims[0], a.dD, nullptr, nullptr, EPI_STORE);
+}
+
+}  // namespace nb

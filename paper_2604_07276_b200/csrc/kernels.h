@@ -1,0 +1,176 @@
+// Kernel argument structs and host launch wrappers of nnmd_b200.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nb {
+
+// Number of kernels launched by this library in the process (for the bench's launch count).
+void count_launch();
+long long launch_count();
+
+// ---------------------------------------------------------------- DD build -----------
+struct SysArgs {
+  const double* pos;      // 3n, wrapped on periodic axes
+  const int* species;     // n
+  const int64_t* gid;     // n
+  int n;
+  double L[3];
+  int per[3];
+  int n_species;
+};
+
+struct RankArgs {
+  int rank;
+  int dims[3];
+  double lo[3], hi[3];   // subdomain (make_subdomain, decomp.cpp:80-94)
+  double slab_lo[3], slab_hi[3];   // lo - t - guard, hi + t + guard (decomp.cpp:104-108)
+  double rc_lo[3], rc_hi[3];       // rc slab (first-layer test, decomp.cpp:317-321)
+  int wide;              // 1: wide_halo (first-layer ghosts are centres)
+};
+
+// err[0]: first atom with an unwrapped position / bad species (atomicMin), err[1]: first
+// centre whose neighbour count exceeds n_max (atomicMin), err[2]: first ghost target whose
+// reverse list overflows.  Initialised to INT_MAX.
+void launch_owner(const SysArgs& s, const int dims[3], int* owner, int* err, cudaStream_t st);
+void launch_dd_flags(const SysArgs& s, const RankArgs& r, const int* owner, int* is_local,
+                     int* gcount, cudaStream_t st);
+// exclusive scan of n ints; out[n] receives the total (out has n+1 entries)
+void launch_scan(const int* in, int* out, int n, cudaStream_t st);
+void launch_dd_members(const SysArgs& s, const RankArgs& r, const int* owner, const int* loc_off,
+                       const int* gh_off, int n_atoms, int* m_atom, int* m_shift, double* m_pos,
+                       int* m_owner, cudaStream_t st);
+// centre flags over members (locals always; first-layer ghosts when wide)
+void launch_centre_flags(const RankArgs& r, const int* counts /*[nloc, ngh]*/, const double* m_pos,
+                         int n_members_cap, int* flag, cudaStream_t st);
+void launch_centre_compact(const int* flag, const int* off, int n_members, int* cen_member,
+                           int* cidx, cudaStream_t st);
+
+// ---------------------------------------------------------------- cells / neighbours -
+struct CellArgs {
+  double origin[3], width[3];
+  int dims[3];
+};
+void launch_cell_count(const CellArgs& c, const double* m_pos, int n_members, int* m_cell,
+                       int* cell_count, cudaStream_t st);
+void launch_cell_fill(const int* m_cell, int n_members, const int* cell_start, int* cell_fill,
+                      int* cell_members, cudaStream_t st);
+
+struct NbrArgs {
+  const double* pos;
+  const int* species;
+  const int64_t* gid;
+  double L[3];
+  const int* m_atom;
+  const int* m_shift;
+  const int* m_cell;
+  const int* cell_start;
+  const int* cell_members;
+  int cdims[3];
+  const int* centre_member;  // member index of each list owner (NULL: li + member_offset)
+  int member_offset;
+  int n_lists;
+  int cand_limit;            // only candidate members with index < cand_limit
+  int n_max;
+  double rc2;
+  int* nlist;                // [n_lists][n_max] member indices, canonical order
+  int* nn;                   // [n_lists]
+  int* err;                  // &err[slot]: atomicMin of the owner atom of an overflowing list
+  int* nonempty;             // optional: count of lists with >= 1 row (route entries)
+};
+void launch_neighbors(const NbrArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------- forces --------------
+struct ForceArgs {
+  const int* nlist;
+  const int* nn;
+  int n_max;
+  const int* cidx;       // member -> centre index, -1 if not a centre
+  const int* rlist;      // ghost reverse lists (masked), [n_ghost][n_max]
+  const int* rn;
+  int nloc;
+  int n_targets;         // masked: all members; wide: locals
+  const double* g;       // [centre][n_max][3] row gradients de/dd_k
+  double* fmem;          // [member][3] force partial
+};
+void launch_force_gather(const ForceArgs& a, cudaStream_t st);
+
+struct AssembleArgs {
+  int n_atoms;
+  int rank;
+  int wide;
+  const int* owner;
+  const int* loc_off;    // exclusive prefix of locals per atom
+  const int* gh_off;     // exclusive prefix of ghosts per atom (n+1 entries)
+  const int* counts;     // [nloc, ngh]
+  const double* fmem;
+  const double* e_centre;  // centre energies
+  double* out;           // [E, W9, F(3n), ae(n)]
+};
+void launch_assemble(const AssembleArgs& a, cudaStream_t st);
+// E += sum_{c < nloc} e[c]; W += sum vir[c]  (deterministic single-block reduction)
+void launch_energy_virial(const double* e_centre, const double* vir, const int* counts,
+                          double* out, cudaStream_t st);
+
+// ---------------------------------------------------------------- network -------------
+constexpr int kMaxLayers = 8;
+struct DpArgs {
+  // model
+  int M, mr, n_max, ns, n_embed, n_attn, n_fit;
+  int edims[kMaxLayers];          // output width of each embed layer
+  int fdims[kMaxLayers + 1];      // fit widths, fdims[0] = M*mr
+  const float* w0;
+  const float* ctab;
+  const float* ew[kMaxLayers];
+  const float* eb[kMaxLayers];
+  const float* ab[16];
+  const float* fw[kMaxLayers];
+  const float* fb[kMaxLayers];
+  double rc, rcs;
+  float inv_sqrt_nmax;
+  // system
+  const double* pos;
+  const int* species;
+  double L[3];
+  // rank
+  const int* m_atom;
+  const int* m_shift;
+  const int* cen_member;
+  int n_centres;
+  const int* nlist;
+  const int* nn;
+  // stash (per centre) and scratch (per CTA slot)
+  float* X;             // [n_attn+1][n_centres][n_max][M]
+  size_t x_layer_stride;
+  float4* R;            // [n_centres][n_max]
+  float* Ad;            // [n_centres][M*4]
+  float* Bd;            // [n_centres][4*mr]
+  float* D;             // [n_centres][M*mr]
+  float* dD;            // [n_centres][M*mr]
+  double* g;            // [n_centres][n_max][3]
+  double* vir;          // [n_centres][9]
+  float* scratch;
+  size_t scratch_slot;  // floats per CTA slot
+};
+size_t dp_scratch_floats(const DpArgs& a);
+size_t dp_smem_bytes(const DpArgs& a);
+void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st);
+void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st);
+
+// Fitting net over all centres (batched GEMMs): Y[l] activations, e (double) energies,
+// then dD = de/dD.
+struct FitArgs {
+  int n_fit;
+  int fdims[kMaxLayers + 1];
+  const float* fw[kMaxLayers];
+  const float* fb[kMaxLayers];
+  int n_centres;
+  const float* D;
+  float* Y[kMaxLayers];      // hidden activations [n_centres][fdims[l+1]]
+  float* delta[2];           // ping-pong [n_centres][max width]
+  double* e;                 // [n_centres]
+  float* dD;
+};
+void launch_fit(const FitArgs& a, cudaStream_t st);
+
+}  // namespace nb

@@ -1,0 +1,194 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden vectors and
+the CPU oracle.  Bit-exact for neighbour rows and halo sets; FP32 network tolerance 1e-5
+relative for energy (|dE|/|E|), forces (max|dF| / max|F|) and virial (max|dW| / max|W|)."""
+import numpy as np
+import pytest
+
+import paper_2604_07276_b200 as nb
+import oracle as O
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+CASES = ["dd_case_0", "dd_case_1", "dd_case_2"]
+TOL = 1e-5  # FP32 contractions vs the FP64 reference
+
+
+def rel_err(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
+
+
+def make_test_model(case_g):
+    return nb.init_model(nb.test_spec(float(case_g["rc"])), int(case_g["model_seed"]))
+
+
+def rows_by_centre(g):
+    off = np.concatenate([[0], np.cumsum(g["row_counts"])])
+    return [(g["row_member"][off[i]:off[i + 1]], g["row_image"][off[i]:off[i + 1]]) for i in range(len(g["row_counts"]))]
+
+
+def check_rows(ev, rank, n_max, golden_rows):
+    ca, idx, img, cnt = ev.debug_nlist(rank, n_max)
+    for c, atom in enumerate(ca):
+        gm, gi = golden_rows[atom]
+        assert cnt[c] == len(gm), (rank, atom)
+        assert np.array_equal(idx[c, : cnt[c]], gm), (rank, atom)
+        assert np.array_equal(img[c, : cnt[c]], gi), (rank, atom)
+    return ca
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_single_domain_rows_bitexact_and_energy(case):
+    g = load_golden(case)
+    m = make_test_model(g)
+    ev = nb.DeviceEvaluator(m, n_ranks=1)
+    ev.set_debug(True)
+    r = ev.compute(g["pos"], g["species"], g["box"])
+    ca = check_rows(ev, 0, 64, rows_by_centre(g))
+    assert np.array_equal(ca, np.arange(len(g["pos"])))
+    assert abs(r["energy"] - g["energy"]) / abs(g["energy"]) <= TOL
+    assert rel_err(r["forces"], g["forces"]) <= TOL
+    assert rel_err(r["virial"], g["virial"]) <= TOL
+    assert rel_err(r["atom_energy"], g["atom_energy"]) <= TOL
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("scheme,tag", [(nb.MASKED_REDUCTION, "masked"), (nb.WIDE_HALO, "wide")])
+@pytest.mark.parametrize("nr", [1, 2, 4, 8])
+def test_dd_rows_halo_forces(case, scheme, tag, nr):
+    g = load_golden(case)
+    m = make_test_model(g)
+    ev = nb.DeviceEvaluator(m, n_ranks=nr, scheme=scheme)
+    ev.set_debug(True)
+    r = ev.compute(g["pos"], g["species"], g["box"])
+    grows = rows_by_centre(g)
+    for rank in range(nr):
+        atom, own, sh = ev.debug_ghosts(rank)
+        assert np.array_equal(atom, g[f"halo_{tag}_R{nr}_r{rank}_atom"])
+        assert np.array_equal(own, g[f"halo_{tag}_R{nr}_r{rank}_owner"])
+        assert np.array_equal(sh, g[f"halo_{tag}_R{nr}_r{rank}_shift"])
+        check_rows(ev, rank, 64, grows)
+        st = ev.rank_stats(rank)
+        gs = g[f"dd_{tag}_R{nr}_stats"][rank]
+        assert (st["locals"], st["ghosts"], st["centers"]) == tuple(gs[:3])
+    e_ref = float(g[f"dd_{tag}_R{nr}_energy"])
+    assert abs(r["energy"] - e_ref) / abs(e_ref) <= TOL
+    assert rel_err(r["forces"], g[f"dd_{tag}_R{nr}_forces"]) <= TOL
+    assert rel_err(r["atom_energy"], g[f"dd_{tag}_R{nr}_atom_energy"]) <= TOL
+    assert rel_err(r["virial"], g["virial"]) <= TOL
+
+
+def test_paper_model_small_system():
+    g = load_golden("paper_small")
+    m = nb.init_model(nb.paper_spec(6.0), 1)
+    ev = nb.DeviceEvaluator(m, n_ranks=1)
+    ev.set_debug(True)
+    r = ev.compute(g["pos"], g["species"], g["box"])
+    check_rows(ev, 0, 160, rows_by_centre(g))
+    print("paper_small: dE/E", abs(r["energy"] - g["energy"]) / abs(g["energy"]),
+          "dF", rel_err(r["forces"], g["forces"]), "dW", rel_err(r["virial"], g["virial"]))
+    assert abs(r["energy"] - g["energy"]) / abs(g["energy"]) <= TOL
+    assert rel_err(r["forces"], g["forces"]) <= TOL
+    assert rel_err(r["virial"], g["virial"]) <= TOL
+    ev2 = nb.DeviceEvaluator(m, n_ranks=2)
+    r2 = ev2.compute(g["pos"], g["species"], g["box"])
+    assert abs(r2["energy"] - g["dd_masked_R2_energy"]) / abs(g["energy"]) <= TOL
+    assert rel_err(r2["forces"], g["dd_masked_R2_forces"]) <= TOL
+    # per-centre energies are rank-count invariant bit for bit (same rows, same kernel)
+    assert np.array_equal(r2["atom_energy"], r["atom_energy"])
+
+
+def test_overflow_names_atom_id():
+    g = load_golden("overflow_atom7")
+    m = nb.init_model(nb.test_spec(1.5, 2, 0), 12345)
+    m.set_n_max(2)
+    ev = nb.DeviceEvaluator(m)
+    with pytest.raises(nb.CapacityError, match="atom id 7"):
+        ev.compute(g["pos"], g["species"], g["box"], gids=g["gids"])
+
+
+def test_unwrapped_and_bad_species_rejected():
+    g = load_golden("dd_case_0")
+    m = make_test_model(g)
+    ev = nb.DeviceEvaluator(m)
+    pos = g["pos"].copy()
+    pos[3, 1] = -0.1
+    with pytest.raises(nb.Error, match="wrapped"):
+        ev.compute(pos, g["species"], g["box"])
+    sp = g["species"].copy()
+    sp[5] = 9
+    with pytest.raises(nb.Error, match="species"):
+        ev.compute(g["pos"], sp, g["box"])
+    # the context stays usable after an input error
+    r = ev.compute(g["pos"], g["species"], g["box"])
+    assert abs(r["energy"] - g["energy"]) / abs(g["energy"]) <= TOL
+
+
+def test_isolated_atom_energy_is_fit_of_zero():
+    m = nb.init_model(nb.test_spec(1.5, 2, 1), 99)
+    port = O.Port()
+    h = port.model_init(O.test_spec(1.5, 2, 1), 99)
+    box = np.array([12.0, 12.0, 12.0])
+    pos = np.array([[6.0, 6.0, 6.0]])
+    sp = np.array([0], dtype=np.int32)
+    r = nb.DeviceEvaluator(m).compute(pos, sp, box)
+    o = port.evaluate(h, pos, sp, box)
+    assert r["energy"] == pytest.approx(o["energy"], rel=1e-6)
+    assert np.all(r["forces"] == 0.0)
+
+
+def test_translation_invariance_and_momentum():
+    g = load_golden("paper_small")
+    m = nb.init_model(nb.paper_spec(6.0), 1)
+    ev = nb.DeviceEvaluator(m)
+    r0 = ev.compute(g["pos"], g["species"], g["box"])
+    L = g["box"][0]
+    moved = np.mod(g["pos"] + np.array([0.37, -0.21, 0.11]), L)
+    r1 = ev.compute(moved, g["species"], g["box"])
+    assert abs(r1["energy"] - r0["energy"]) / abs(r0["energy"]) <= TOL
+    assert rel_err(r1["forces"], r0["forces"]) <= TOL
+    assert np.abs(r0["forces"].sum(axis=0)).max() <= 1e-6 * np.abs(r0["forces"]).max() * len(g["pos"]) ** 0.5
+    W = r0["virial"]
+    assert np.abs(W - W.T).max() <= 1e-5 * np.abs(W).max()
+
+
+def test_provider_species_map_and_group_mask():
+    g = load_golden("dd_case_1")
+    m = make_test_model(g)
+    n = len(g["pos"])
+    atoms = nb.AtomSet(np.arange(n), g["species"], g["pos"])
+    box = nb.SimBox(g["box"])
+    p = nb.DpProvider(m, nb.DpProvider.Options(decomposed=True, scheme=nb.WIDE_HALO, n_ranks=2))
+    res = p.evaluate(atoms, box)
+    assert abs(res.energy - g["energy"]) / abs(g["energy"]) <= TOL
+    assert rel_err(res.forces, g["forces"]) <= TOL
+    mask = np.zeros(n, dtype=bool)
+    mask[: n // 2] = True
+    pm = nb.DpProvider(m, nb.DpProvider.Options(), group_mask=mask)
+    rm = pm.evaluate(atoms, box)
+    assert np.all(rm.forces[n // 2:] == 0.0)
+    with pytest.raises(nb.Error, match="species map"):
+        nb.DpProvider(m, nb.DpProvider.Options(species_map=[0, 1])).evaluate(atoms, box)
+
+
+def test_full_size_1hci_properties():
+    """15,668-atom C1 system: rank-count invariance of per-centre energies (bitwise), force
+    sum, virial symmetry, and oracle spot checks of per-centre energies."""
+    box, pos, sp = nb.synth_system(15668, 0.1, 0.9, 1)
+    m = nb.init_model(nb.paper_spec(6.0), 1)
+    r1 = nb.DeviceEvaluator(m, n_ranks=1).compute(pos, sp, box)
+    r8 = nb.DeviceEvaluator(m, n_ranks=8).compute(pos, sp, box)
+    assert np.array_equal(r1["atom_energy"], r8["atom_energy"])
+    assert rel_err(r8["forces"], r1["forces"]) <= 1e-9
+    fmax = np.abs(r1["forces"]).max()
+    assert np.abs(r1["forces"].sum(axis=0)).max() <= 1e-6 * fmax * len(pos) ** 0.5
+    W = r1["virial"]
+    assert np.abs(W - W.T).max() <= 1e-5 * np.abs(W).max()
+    port = O.Port()
+    h = port.model_init(O.PAPER_SPEC, 1)
+    counts, mem, img, d = port.neighbor_rows(h, pos, sp, box)
+    off = np.concatenate([[0], np.cumsum(counts)])
+    for c in (0, 4321, 15667):
+        rows = slice(off[c], off[c + 1])
+        e, _ = port.evaluate_center(h, int(sp[c]), d[rows], sp[mem[rows]])
+        assert abs(r1["atom_energy"][c] - e) <= TOL * max(abs(e), 1e-3)
+    port.model_free(h)
