@@ -217,8 +217,9 @@ def run_ours(args, ws, rank, local):
     uid = nb.DeviceEvaluator.nccl_unique_id() if (ws > 1 and rank == 0) else None
     uid = bcast_bytes(uid, ws) if ws > 1 else None
     scheme = nb.WIDE_HALO if args.scheme == "wide" else nb.MASKED_REDUCTION
+    prec = {"fp32": nb.PREC_FP32, "tf32": nb.PREC_TF32, "simt": nb.PREC_FP32_SIMT}[args.precision]
     ev = nb.DeviceEvaluator(model, n_ranks=ws, scheme=scheme, device=local, world_size=ws, world_rank=rank,
-                            nccl_id=uid)
+                            nccl_id=uid, precision=prec)
     stream = torch.cuda.ExternalStream(ev.stream(), device=dev)
     d_pos = torch.from_numpy(pos).to(dev)
     d_sp = torch.from_numpy(sp).to(dev)
@@ -267,6 +268,7 @@ def run_ours(args, ws, rank, local):
     ev.set_debug(False)
     f_fwd, f_bwd = algorithmic_flops(cnt)
     x_fwd, x_bwd = executed_flops(cnt)
+    npass = {"fp32": 3, "tf32": 1, "simt": 1}[args.precision]
     k_bwd = kernel_acc.get("centre_backward", 0.0) / args.steps
     k_fwd = kernel_acc.get("centre_forward", 0.0) / args.steps
     peaks = {}
@@ -302,19 +304,21 @@ def run_ours(args, ws, rank, local):
             "metric": "MD steps/s (DPA-1 force evaluation per step)", "value": value, "unit": "steps/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic solvated protein (nnmd_synth_system seed 1), random-init DPA-1 weights (init_model seed 1)",
+            "dtype": {"fp32": "f32 (3xTF32 tcgen05)", "tf32": "tf32", "simt": "f32 (SIMT)"}[args.precision], "data": "synthetic solvated protein (nnmd_synth_system seed 1), random-init DPA-1 weights (init_model seed 1)",
             "ns_per_day": ns_per_day(value),
             "config": {"workload": f"1HCI-sized solvated protein, {n} atoms, DPA-1 1.58M params, rc={args.rc} A, "
                                    f"{'weak' if args.weak else 'strong'} DD over {ws} GPU(s)",
                        "n_atoms": n, "rc": args.rc, "n_max": nb.paper_spec(args.rc).n_max,
                        "dd_ranks": ws, "scheme": args.scheme, "l2": "flushed between steps (256 MB write)",
-                       "precision": "fp32 network (SIMT), fp64 geometry/forces"},
+                       "precision": {"fp32": "3xTF32 tcgen05 (FP32-grade, tol 1e-5)", "tf32": "1xTF32 tcgen05 (tol 2e-3)",
+                                     "simt": "FP32 SIMT (tol 1e-5)"}[args.precision] + "; fp64 geometry/forces"},
             "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ns_per_day": ns_per_day(e2e)},
             "roofline": {"bound": "tensor", "kernel": "k_centre_backward", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                          "algorithmic_flop_per_launch": f_bwd, "ms_per_launch": k_bwd,
-                         "executed_tflops": x_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0,
+                         "executed_tflops": npass * x_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0,
+                         "mma_passes": npass,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                          "forward": {"ms_per_launch": k_fwd, "algorithmic_flop": f_fwd,
                                      "achieved_tflops": f_fwd / (k_fwd * 1e-3) / 1e12 if k_fwd > 0 else 0.0}},
@@ -340,6 +344,8 @@ def main():
     ap.add_argument("--scheme", choices=["masked", "wide"], default="masked")
     ap.add_argument("--ref-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", choices=["fp32", "tf32", "simt"], default="fp32",
+                    help="fp32 = 3xTF32 tcgen05 (FP32-grade, default); tf32 = 1xTF32 tcgen05; simt = CUDA-core FP32")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
     if args.impl == "reference":

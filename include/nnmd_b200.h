@@ -45,8 +45,13 @@ typedef struct {
 
 /* DdScheme (decomp.hpp:128-129). */
 enum { NNMD_MASKED_REDUCTION = 0, NNMD_WIDE_HALO = 1 };
-/* Arithmetic of the dense contractions. */
-enum { NNMD_PREC_FP32 = 0 };
+/* Arithmetic of the dense contractions (all accumulate in FP32; geometry, row gradients,
+ * forces, energies and virial are FP64):
+ *   NNMD_PREC_FP32      3xTF32 on tcgen05 tensor cores (hi/lo split) -- FP32-grade,
+ *                       parity tolerance 1e-5 relative (default)
+ *   NNMD_PREC_TF32      1xTF32 on tcgen05 -- stated tolerance 2e-3 relative
+ *   NNMD_PREC_FP32_SIMT plain FP32 FMA on CUDA cores (validation path) -- 1e-5 */
+enum { NNMD_PREC_FP32 = 0, NNMD_PREC_TF32 = 1, NNMD_PREC_FP32_SIMT = 2 };
 
 typedef struct {
   int n_ranks;    /* DD ranks (partition_ranks); 1 = one domain (== evaluate_dp bit-for-bit rows) */
@@ -119,6 +124,11 @@ nnmd_status nnmd_b200_debug_nlist(const nnmd_b200* ctx, int rank, int* n_centres
 nnmd_status nnmd_b200_debug_ghosts(const nnmd_b200* ctx, int rank, int* n_ghosts,
                                    int32_t* atom, int32_t* owner, int32_t* shift);
 
+/* Self-test of the in-kernel block GEMM (one CTA) on host buffers: C[M x N] = op(A) op(B),
+ * A is [M x K] (ta=0) or [K x M] (ta=1), B is [K x N] (tb=0) or [N x K] (tb=1);
+ * mode 0 SIMT FP32, 1 3xTF32 tcgen05, 2 1xTF32 tcgen05. */
+nnmd_status nnmd_b200_selftest_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A,
+                                    const float* B, float* C);
 /* Total kernels launched by this library in this process (bench launch accounting). */
 long long nnmd_b200_launch_count(void);
 /* Device stream of the context (cudaStream_t), for external event timing. */

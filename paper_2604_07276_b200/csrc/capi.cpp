@@ -239,3 +239,28 @@ nnmd_status nnmd_synth_system(int64_t n, double rho, double min_sep, uint64_t se
 }  // extern "C"
 
 extern "C" long long nnmd_b200_launch_count(void) { return nb::launch_count(); }
+
+extern "C" nnmd_status nnmd_b200_selftest_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A,
+                                               const float* B, float* C) {
+  return guarded([&] {
+    nb::require(M >= 0 && N >= 0 && K >= 0 && mode >= 0 && mode <= 2, "selftest_gemm: bad arguments");
+    const int lda = ta ? M : K, ldb = tb ? K : N;
+    float *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    auto chk = [](cudaError_t e) {
+      if (e != cudaSuccess) throw nb::CudaError(std::string("selftest_gemm: ") + cudaGetErrorString(e));
+    };
+    chk(cudaMalloc(&dA, sizeof(float) * (static_cast<size_t>(M) * K + 1)));
+    chk(cudaMalloc(&dB, sizeof(float) * (static_cast<size_t>(K) * N + 1)));
+    chk(cudaMalloc(&dC, sizeof(float) * (static_cast<size_t>(M) * N + 1)));
+    chk(cudaMemcpy(dA, A, sizeof(float) * static_cast<size_t>(M) * K, cudaMemcpyHostToDevice));
+    chk(cudaMemcpy(dB, B, sizeof(float) * static_cast<size_t>(K) * N, cudaMemcpyHostToDevice));
+    chk(cudaMemset(dC, 0, sizeof(float) * static_cast<size_t>(M) * N));
+    nb::selftest_gemm(mode, ta, tb, M, N, K, dA, lda, dB, ldb, dC);
+    chk(cudaGetLastError());
+    chk(cudaDeviceSynchronize());
+    chk(cudaMemcpy(C, dC, sizeof(float) * static_cast<size_t>(M) * N, cudaMemcpyDeviceToHost));
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dC);
+  });
+}

@@ -90,7 +90,8 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   model_.validate();
   require(o.n_ranks >= 1, "nnmd_b200: n_ranks must be >= 1");
   require(o.scheme == NNMD_MASKED_REDUCTION || o.scheme == NNMD_WIDE_HALO, "nnmd_b200: bad scheme");
-  require(o.precision == NNMD_PREC_FP32, "nnmd_b200: unsupported precision");
+  require(o.precision == NNMD_PREC_FP32 || o.precision == NNMD_PREC_TF32 || o.precision == NNMD_PREC_FP32_SIMT,
+          "nnmd_b200: unsupported precision");
   require(o.world_size >= 1 && o.world_rank >= 0 && o.world_rank < o.world_size,
           "nnmd_b200: bad world_size/world_rank");
   require(model_.na <= 16 && model_.embed.size() <= kMaxLayers && model_.fit.size() <= kMaxLayers,
@@ -431,7 +432,8 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.dD = dD_.p;
   dp.g = g_.p;
   dp.vir = vir_.p;
-  const int grid = std::max(1, std::min(ncen, 2 * n_sm_));
+  dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
+  const int grid = std::max(1, std::min(ncen, (dp.mode == 0 ? 2 : 1) * n_sm_));
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
   scratch_.ensure(dp.scratch_slot * grid);
   dp.scratch = scratch_.p;
@@ -466,6 +468,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   fa.delta[1] = fitd_.p + static_cast<size_t>(maxw) * ncen;
   fa.e = e_.p;
   fa.dD = dD_.p;
+  fa.mode = dp.mode;
   tic("fit");
   launch_fit(fa, st_);
   toc();

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "kernels.h"
+#include "tc_gemm.cuh"
 
 namespace nb {
 
@@ -60,8 +61,32 @@ __device__ inline Slot slot_of(const DpArgs& a, float* base) {
   return s;
 }
 
-struct Smem {
+// GEMM policy: MODE 0 = SIMT FP32 (gemm_simt.cuh), 1 = 3xTF32 tcgen05, 2 = 1xTF32 tcgen05.
+template <int MODE>
+struct Mm {
   GemmSmem* gs;
+  tc::State st;
+  __device__ void init(unsigned char* head) {
+    if constexpr (MODE == 0) gs = reinterpret_cast<GemmSmem*>(head);
+    else tc::init(st, reinterpret_cast<tc::Smem*>(head));
+  }
+  __device__ void finish() {
+    if constexpr (MODE != 0) tc::finish(st);
+  }
+  template <bool TA, bool TB, class Epi>
+  __device__ __forceinline__ void run(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                                      Epi epi) {
+    if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
+    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1>(st, M, N, K, A, lda, B, ldb, epi);
+  }
+};
+
+__host__ __device__ inline size_t head_bytes(int mode) {
+  return mode == 0 ? sizeof(GemmSmem) : sizeof(tc::Smem);
+}
+
+struct Smem {
+  unsigned char* head;
   float4* R;
   float4* dR;
   float* s;
@@ -76,7 +101,7 @@ struct Smem {
   double* red;
 };
 
-__host__ __device__ inline size_t smem_layout(const DpArgs& a, unsigned char* base, Smem* out) {
+__host__ __device__ inline size_t smem_layout(const DpArgs& a, int mode, unsigned char* base, Smem* out) {
   size_t o = 0;
   auto take = [&](size_t bytes) {
     o = (o + 15) & ~size_t(15);
@@ -85,7 +110,7 @@ __host__ __device__ inline size_t smem_layout(const DpArgs& a, unsigned char* ba
     return p;
   };
   Smem s;
-  s.gs = reinterpret_cast<GemmSmem*>(take(sizeof(GemmSmem)));
+  s.head = take(head_bytes(mode));
   s.R = reinterpret_cast<float4*>(take(sizeof(float4) * a.n_max));
   s.dR = reinterpret_cast<float4*>(take(sizeof(float4) * a.n_max));
   s.s = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
@@ -138,7 +163,8 @@ __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int
 
 // Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
 // Writes intermediate activations to EMB and the last to `out` (n x M).
-__device__ void embed_forward(const DpArgs& a, int n, int zi, const Smem& sm, const Slot& sl,
+template <int MODE>
+__device__ void embed_forward(Mm<MODE>& mm, const DpArgs& a, int n, int zi, const Smem& sm, const Slot& sl,
                               float* out) {
   const int E0 = a.edims[0];
   float* cur = (a.n_embed == 1) ? out : sl.EMB;
@@ -153,7 +179,7 @@ __device__ void embed_forward(const DpArgs& a, int n, int zi, const Smem& sm, co
     const int Ein = a.edims[e - 1], Eout = a.edims[e];
     float* nxt = (e + 1 == a.n_embed) ? out : sl.EMB + off;
     const float* b = a.eb[e];
-    bgemm<false, true>(n, Eout, Ein, cur, Ein, a.ew[e], Ein, *sm.gs,
+    mm.template run<false, true>(n, Eout, Ein, cur, Ein, a.ew[e], Ein,
                        [&](int m, int o, float v) { nxt[m * Eout + o] = tanhf(v + b[o]); });
     __syncthreads();
     cur = nxt;
@@ -195,15 +221,19 @@ size_t dp_scratch_floats(const DpArgs& a) {
   return align4(nm * M2) * 2 + align4(nm * nm) * 4 + align4(nm * W) * 2 + emb_floats(a) + 64;
 }
 
-size_t dp_smem_bytes(const DpArgs& a) { return smem_layout(a, nullptr, nullptr) + 16; }
+size_t dp_smem_bytes(const DpArgs& a, int mode) { return smem_layout(a, mode, nullptr, nullptr) + 1024; }
 
 // ------------------------------------------------------------------------------------
 // Forward: rows -> embedding -> attention layers -> descriptor D = (X^T R)(R^T X_<) / n_max
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_centre_forward(const __grid_constant__ DpArgs a) {
-  extern __shared__ __align__(16) unsigned char dp_smem[];
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) k_centre_forward(const __grid_constant__ DpArgs a) {
+  extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
+  unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
   Smem sm;
-  smem_layout(a, dp_smem, &sm);
+  smem_layout(a, MODE, dp_smem, &sm);
+  Mm<MODE> mm;
+  mm.init(sm.head);
   const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
@@ -214,19 +244,19 @@ __global__ void __launch_bounds__(256) k_centre_forward(const __grid_constant__ 
     float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
     for (int k = threadIdx.x; k < n; k += blockDim.x) Rg[k] = sm.R[k];
     float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
-    embed_forward(a, n, zi, sm, sl, X);
+    embed_forward(mm, a, n, zi, sm, sl, X);
     for (int l = 0; l < a.n_attn; ++l) {
       const float* Xl = X + l * a.x_layer_stride;
       float* Xn = X + (l + 1) * a.x_layer_stride;
-      bgemm<false, false>(n, M2, M, Xl, M, a.ab[l], M2, *sm.gs,
+      mm.template run<false, false>(n, M2, M, Xl, M, a.ab[l], M2,
                           [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
       __syncthreads();
-      bgemm<false, true>(n, n, M, sl.U, M2, Xl, M, *sm.gs,
+      mm.template run<false, true>(n, n, M, sl.U, M2, Xl, M,
                          [&](int k, int j, float v) { sl.PU[k * n + j] = v; });
       __syncthreads();
       softmax_gate(n, sl.PU, nullptr, sl.PT, inv_sig, sm);
       __syncthreads();
-      bgemm<false, false>(n, M, n, sl.PT, n, sl.U + M, M2, *sm.gs,
+      mm.template run<false, false>(n, M, n, sl.PT, n, sl.U + M, M2,
                           [&](int k, int m, float v) { Xn[k * M + m] = Xl[k * M + m] + v; });
       __syncthreads();
     }
@@ -256,17 +286,21 @@ __global__ void __launch_bounds__(256) k_centre_forward(const __grid_constant__ 
     for (int idx = threadIdx.x; idx < M * 4; idx += blockDim.x) a.Ad[static_cast<size_t>(c) * M * 4 + idx] = sm.Ad[idx];
     for (int idx = threadIdx.x; idx < 4 * mr; idx += blockDim.x) a.Bd[static_cast<size_t>(c) * 4 * mr + idx] = sm.Bd[idx];
     __syncthreads();
-  }
+  }  mm.finish();
 }
 
 // ------------------------------------------------------------------------------------
 // Backward: dD -> (dA, dB) -> dX, dR -> attention layers in reverse -> embedding ->
 // row gradients g_k = de/dd_k (FP64 geometry), per-centre virial -sum g (x) d.
 // ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_centre_backward(const __grid_constant__ DpArgs a) {
-  extern __shared__ __align__(16) unsigned char dp_smem[];
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) k_centre_backward(const __grid_constant__ DpArgs a) {
+  extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
+  unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
   Smem sm;
-  smem_layout(a, dp_smem, &sm);
+  smem_layout(a, MODE, dp_smem, &sm);
+  Mm<MODE> mm;
+  mm.init(sm.head);
   const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -320,16 +354,16 @@ __global__ void __launch_bounds__(256) k_centre_backward(const __grid_constant__
     for (int l = a.n_attn - 1; l >= 0; --l) {
       const float* Xl = X + l * a.x_layer_stride;
       const float* AB = a.ab[l];
-      bgemm<false, false>(n, M2, M, Xl, M, AB, M2, *sm.gs,
+      mm.template run<false, false>(n, M2, M, Xl, M, AB, M2,
                           [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
       __syncthreads();
-      bgemm<false, true>(n, n, M, sl.U, M2, Xl, M, *sm.gs,
+      mm.template run<false, true>(n, n, M, sl.U, M2, Xl, M,
                          [&](int k, int j, float v) { sl.PU[k * n + j] = v; });
       __syncthreads();
       softmax_gate(n, sl.PU, sl.PU, sl.PT, inv_sig, sm);
       __syncthreads();
       // T = dP~ = dY U_B^T
-      bgemm<false, true>(n, n, M, dY, M, sl.U + M, M2, *sm.gs,
+      mm.template run<false, true>(n, n, M, dY, M, sl.U + M, M2,
                          [&](int k, int j, float v) { sl.T[k * n + j] = v; });
       __syncthreads();
       // row pass: dP = dP~ Theta, dC = dP~ P / sigma, t_k, dsigma partials
@@ -401,16 +435,16 @@ __global__ void __launch_bounds__(256) k_centre_backward(const __grid_constant__
       }
       __syncthreads();
       // dU_A = dS X ; dU_B = P~^T dY
-      bgemm<false, false>(n, M, n, sl.T, n, Xl, M, *sm.gs,
+      mm.template run<false, false>(n, M, n, sl.T, n, Xl, M,
                           [&](int k, int m, float v) { sl.dU[k * M2 + m] = v; });
-      bgemm<true, false>(n, M, n, sl.PT, n, dY, M, *sm.gs,
+      mm.template run<true, false>(n, M, n, sl.PT, n, dY, M,
                          [&](int k, int m, float v) { sl.dU[k * M2 + M + m] = v; });
       __syncthreads();
       // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T
-      bgemm<true, false>(n, M, n, sl.T, n, sl.U, M2, *sm.gs,
+      mm.template run<true, false>(n, M, n, sl.T, n, sl.U, M2,
                          [&](int k, int m, float v) { dXn[k * M + m] = dY[k * M + m] + v; });
       __syncthreads();
-      bgemm<false, true>(n, M, M2, sl.dU, M2, AB, M2, *sm.gs,
+      mm.template run<false, true>(n, M, M2, sl.dU, M2, AB, M2,
                          [&](int k, int m, float v) { dXn[k * M + m] += v; });
       __syncthreads();
       float* tmp = dY;
@@ -419,7 +453,7 @@ __global__ void __launch_bounds__(256) k_centre_backward(const __grid_constant__
     }
     // embedding backward (dp_core.hpp:580-596): recompute hidden activations
     if (a.n_embed > 1) {
-      embed_forward(a, n, zi, sm, sl, dXn);  // last layer output discarded (== X_0)
+      embed_forward(mm, a, n, zi, sm, sl, dXn);  // last layer output discarded (== X_0)
     }
     const float* X0 = X;
     for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
@@ -438,7 +472,7 @@ __global__ void __launch_bounds__(256) k_centre_backward(const __grid_constant__
       for (int e = a.n_embed - 1; e >= 1; --e) {
         const int Ein = a.edims[e - 1], Eout = a.edims[e];
         const float* h = sl.EMB + offs[e - 1];
-        bgemm<false, false>(n, Ein, Eout, dY, Eout, a.ew[e], Ein, *sm.gs,
+        mm.template run<false, false>(n, Ein, Eout, dY, Eout, a.ew[e], Ein,
                             [&](int k, int i, float v) {
                               const float y = h[k * Ein + i];
                               dXn[k * Ein + i] = v * (1.f - y * y);
@@ -495,31 +529,39 @@ __global__ void __launch_bounds__(256) k_centre_backward(const __grid_constant__
       }
     }
     __syncthreads();
+  }  mm.finish();
+}
+
+template <int MODE>
+static void set_smem(size_t smem) {
+  static size_t done = 0;
+  if (smem > done) {
+    cudaFuncSetAttribute(k_centre_forward<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_centre_backward<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    done = smem;
   }
 }
 
 void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st) {
   if (a.n_centres == 0) return;
-  const size_t smem = dp_smem_bytes(a);
-  static size_t set = 0;
-  if (smem > set) {
-    cudaFuncSetAttribute(k_centre_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_centre_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    set = smem;
+  const size_t smem = dp_smem_bytes(a, a.mode);
+  switch (a.mode) {
+    case 0: set_smem<0>(smem); k_centre_forward<0><<<grid, 256, smem, st>>>(a); break;
+    case 1: set_smem<1>(smem); k_centre_forward<1><<<grid, 256, smem, st>>>(a); break;
+    default: set_smem<2>(smem); k_centre_forward<2><<<grid, 256, smem, st>>>(a); break;
   }
-  k_centre_forward<<<grid, 256, smem, st>>>(a); count_launch();
+  count_launch();
 }
 
 void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st) {
   if (a.n_centres == 0) return;
-  const size_t smem = dp_smem_bytes(a);
-  static size_t set = 0;
-  if (smem > set) {
-    cudaFuncSetAttribute(k_centre_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_centre_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    set = smem;
+  const size_t smem = dp_smem_bytes(a, a.mode);
+  switch (a.mode) {
+    case 0: set_smem<0>(smem); k_centre_backward<0><<<grid, 256, smem, st>>>(a); break;
+    case 1: set_smem<1>(smem); k_centre_backward<1><<<grid, 256, smem, st>>>(a); break;
+    default: set_smem<2>(smem); k_centre_backward<2><<<grid, 256, smem, st>>>(a); break;
   }
-  k_centre_backward<<<grid, 256, smem, st>>>(a); count_launch();
+  count_launch();
 }
 
 // ------------------------------------------------------------------------------------
@@ -527,25 +569,55 @@ void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st) {
 // ------------------------------------------------------------------------------------
 enum { EPI_STORE = 0, EPI_TANH_BIAS = 1, EPI_DTANH = 2 };
 
-template <bool TB>
-__global__ void __launch_bounds__(256) k_fit_gemm(int M, int N, int K, const float* __restrict__ A,
-                                                  const float* __restrict__ B, int ldb,
-                                                  float* __restrict__ C, const float* __restrict__ bias,
-                                                  const float* __restrict__ Y, int mode) {
-  __shared__ GemmSmem gs;
-  const int m0 = blockIdx.y * kTM, n0 = blockIdx.x * kTN;
-  const int Ms = min(kTM, M - m0), Ns = min(kTN, N - n0);
+// One output tile per CTA: SIMT 64x64 (MODE 0) or tcgen05 128x256 (MODE 1/2).
+template <bool TB, int MODE>
+__global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const float* __restrict__ A,
+                                                     const float* __restrict__ B, int ldb,
+                                                     float* __restrict__ C, const float* __restrict__ bias,
+                                                     const float* __restrict__ Y, int epi_mode) {
+  extern __shared__ __align__(1024) unsigned char fit_smem_raw[];
+  unsigned char* head = fit_smem_raw + ((1024 - (tc::smem_u32(fit_smem_raw) & 1023)) & 1023);
+  constexpr int TM = MODE == 0 ? kTM : tc::kMT;
+  constexpr int TN = MODE == 0 ? kTN : tc::kNT;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  const int Ms = min(TM, M - m0), Ns = min(TN, N - n0);
   const float* Ab = A + static_cast<size_t>(m0) * K;
   const float* Bb = TB ? B + static_cast<size_t>(n0) * ldb : B + n0;
-  bgemm<false, TB>(Ms, Ns, K, Ab, K, Bb, ldb, gs, [&](int m, int n, float v) {
+  Mm<MODE> mm;
+  mm.init(head);
+  mm.template run<false, TB>(Ms, Ns, K, Ab, K, Bb, ldb, [&](int m, int n, float v) {
     const size_t o = static_cast<size_t>(m0 + m) * N + n0 + n;
-    if (mode == EPI_TANH_BIAS) v = tanhf(v + bias[n0 + n]);
-    else if (mode == EPI_DTANH) {
+    if (epi_mode == EPI_TANH_BIAS) v = tanhf(v + bias[n0 + n]);
+    else if (epi_mode == EPI_DTANH) {
       const float y = Y[o];
       v *= 1.f - y * y;
     }
     C[o] = v;
   });
+  mm.finish();
+}
+
+template <bool TB, int MODE>
+static void fit_gemm(int M, int N, int K, const float* A, const float* B, int ldb, float* C, const float* bias,
+                     const float* Y, int epi, cudaStream_t st) {
+  constexpr int TM = MODE == 0 ? kTM : tc::kMT;
+  constexpr int TN = MODE == 0 ? kTN : tc::kNT;
+  const size_t smem = head_bytes(MODE) + 1024;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(k_fit_gemm<TB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set = true;
+  }
+  dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM);
+  k_fit_gemm<TB, MODE><<<grid, 256, smem, st>>>(M, N, K, A, B, ldb, C, bias, Y, epi);
+  count_launch();
+}
+
+template <int MODE>
+static void fit_gemm_tb(bool tb, int M, int N, int K, const float* A, const float* B, int ldb, float* C,
+                        const float* bias, const float* Y, int epi, cudaStream_t st) {
+  if (tb) fit_gemm<true, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st);
+  else fit_gemm<false, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st);
 }
 
 // e[c] = b + w . Y[c]   (linear output layer); delta[c][o] = w[o] (1 - Y[c][o]^2)
@@ -577,10 +649,9 @@ void launch_fit(const FitArgs& a, cudaStream_t st) {
   const int L = a.n_fit;
   auto gemm = [&](bool tb, int N, int K, const float* A, const float* B, int ldb, float* C,
                   const float* bias, const float* Y, int mode) {
-    dim3 grid((N + kTN - 1) / kTN, (nc + kTM - 1) / kTM);
-    if (tb) k_fit_gemm<true><<<grid, 256, 0, st>>>(nc, N, K, A, B, ldb, C, bias, Y, mode);
-    else k_fit_gemm<false><<<grid, 256, 0, st>>>(nc, N, K, A, B, ldb, C, bias, Y, mode);
-    count_launch();
+    if (a.mode == 0) fit_gemm_tb<0>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st);
+    else if (a.mode == 1) fit_gemm_tb<1>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st);
+    else fit_gemm_tb<2>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st);
   };
   // forward hidden layers: Y_l = tanh(X W_l^T + b_l)
   const float* x = a.D;
@@ -608,4 +679,41 @@ void launch_fit(const FitArgs& a, cudaStream_t st) {
   gemm(false, a.fdims[0], a.fdims[1], dcur, a.fw[0], a.fdims[0], a.dD, nullptr, nullptr, EPI_STORE);
 }
 
+}  // namespace nb
+
+namespace nb {
+// ------------------------------------------------------------------------------------
+// Self-test of the block GEMM building blocks (one CTA): C = A(TA) * B(TB).
+// ------------------------------------------------------------------------------------
+template <bool TA, bool TB, int MODE>
+__global__ void __launch_bounds__(256, 1) k_selftest_gemm(int M, int N, int K, const float* A, int lda,
+                                                          const float* B, int ldb, float* C) {
+  extern __shared__ __align__(1024) unsigned char st_smem_raw[];
+  unsigned char* head = st_smem_raw + ((1024 - (tc::smem_u32(st_smem_raw) & 1023)) & 1023);
+  Mm<MODE> mm;
+  mm.init(head);
+  mm.template run<TA, TB>(M, N, K, A, lda, B, ldb, [&](int m, int n, float v) { C[static_cast<size_t>(m) * N + n] = v; });
+  mm.finish();
+}
+
+template <int MODE>
+static void selftest_mode(int ta, int tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                          float* C) {
+  const size_t smem = head_bytes(MODE) + 1024;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<1, 256, smem>>>(M, N, K, A, lda, B, ldb, C);
+  };
+  if (ta && tb) go(k_selftest_gemm<true, true, MODE>);
+  else if (ta) go(k_selftest_gemm<true, false, MODE>);
+  else if (tb) go(k_selftest_gemm<false, true, MODE>);
+  else go(k_selftest_gemm<false, false, MODE>);
+}
+
+void selftest_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A, int lda, const float* B,
+                   int ldb, float* C) {
+  if (mode == 0) selftest_mode<0>(ta, tb, M, N, K, A, lda, B, ldb, C);
+  else if (mode == 1) selftest_mode<1>(ta, tb, M, N, K, A, lda, B, ldb, C);
+  else selftest_mode<2>(ta, tb, M, N, K, A, lda, B, ldb, C);
+}
 }  // namespace nb

@@ -151,9 +151,10 @@ struct DpArgs {
   double* vir;          // [n_centres][9]
   float* scratch;
   size_t scratch_slot;  // floats per CTA slot
+  int mode;             // 0 SIMT FP32, 1 3xTF32 tcgen05, 2 1xTF32 tcgen05
 };
 size_t dp_scratch_floats(const DpArgs& a);
-size_t dp_smem_bytes(const DpArgs& a);
+size_t dp_smem_bytes(const DpArgs& a, int mode);
 void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st);
 void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st);
 
@@ -170,7 +171,12 @@ struct FitArgs {
   float* delta[2];           // ping-pong [n_centres][max width]
   double* e;                 // [n_centres]
   float* dD;
+  int mode;
 };
 void launch_fit(const FitArgs& a, cudaStream_t st);
+
+// One-CTA test of the block GEMM building block (device pointers), mode as DpArgs::mode.
+void selftest_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A, int lda, const float* B,
+                   int ldb, float* C);
 
 }  // namespace nb

@@ -1,0 +1,276 @@
+// Block-level tensor-core GEMM on sm_100a: tcgen05.mma (kind::tf32) with the accumulator
+// in TMEM, operands staged in shared memory in the canonical K-major SWIZZLE_128B layout.
+//
+//   C(m, n) = epi(m, n, sum_k A(m, k) * B(k, n)),  0 <= m < M, 0 <= n < N
+//   A(m, k) = TA ? A[k*lda + m] : A[m*lda + k]        (fp32 in global / L2)
+//   B(k, n) = TB ? B[n*ldb + k] : B[k*ldb + n]
+//
+// Same contract as bgemm (gemm_simt.cuh), so the fused per-centre kernels swap one for
+// the other.  NPASS = 3: FP32-grade "3xTF32" (a_hi b_hi + a_hi b_lo + a_lo b_hi, hi =
+// cvt.rna.tf32(x), lo = x - hi); NPASS = 1: plain TF32.
+//
+// Pipeline (256 threads, one CTA per SM): per 32-wide K chunk all threads load A/B from
+// global (any transposition is absorbed here), split hi/lo, st.shared into the swizzled
+// stage buffer, fence.proxy.async, barrier; thread 0 issues 4 k-steps x NPASS
+// tcgen05.mma (M = 128, N <= 256, K = 8 each) and commits to the stage's mbarrier.  Two
+// stages: loading chunk c+1 overlaps the tensor core working on chunk c.  The epilogue
+// reads the accumulator with tcgen05.ld.32x32b.x16 (warp w owns TMEM lanes
+// 32*(w%4)..+31; warps w and w+4 split the columns).
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace nb {
+namespace tc {
+
+constexpr int kThreads = 256;
+constexpr int kKC = 32;          // K elements per chunk = one 128-byte swizzle row
+constexpr int kMT = 128;         // MMA M
+constexpr int kNT = 256;         // max MMA N per accumulator tile
+constexpr int kTmemCols = 256;
+
+struct alignas(1024) Smem {
+  uint8_t a[2][2][kMT * 128];    // [stage][hi/lo]  16 KB each
+  uint8_t b[2][2][kNT * 128];    // [stage][hi/lo]  32 KB each
+  uint64_t bar[2];
+  uint32_t tmem_base;
+  uint32_t pad;
+};
+
+// Per-CTA pipeline state (identical in every thread).
+struct State {
+  Smem* sm;
+  uint32_t tmem;
+  uint32_t uses[2];     // commits issued per stage
+  uint32_t waited[2];   // commits waited per stage
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (sm_100 "version 1").
+// Rows of 128 bytes, 8-row groups 1024 bytes apart (SBO), LBO unused (1).
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(kMT >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Byte offset of element (row, k) of a K-major SW128 tile (rows of 32 fp32).
+__device__ __forceinline__ uint32_t sw128_off(int row, int k) {
+  return static_cast<uint32_t>(row * 128 + ((((k >> 2) ^ (row & 7)) & 7) << 4) + ((k & 3) << 2));
+}
+
+// Allocate TMEM and initialise the barriers.  Call once per CTA, all threads.
+__device__ __forceinline__ void init(State& st, Smem* sm) {
+  st.sm = sm;
+  st.uses[0] = st.uses[1] = 0;
+  st.waited[0] = st.waited[1] = 0;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm->tmem_base)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 32) {
+    mbar_init(&sm->bar[0], 1);
+    mbar_init(&sm->bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  st.tmem = sm->tmem_base;
+}
+
+__device__ __forceinline__ void finish(State& st) {
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(kTmemCols)
+                 : "memory");
+}
+
+__device__ __forceinline__ void wait_stage(State& st, int s) {
+  while (st.waited[s] < st.uses[s]) {
+    mbar_wait(&st.sm->bar[s], st.waited[s] & 1u);
+    ++st.waited[s];
+  }
+}
+
+template <bool TA, bool TB, int NPASS, class Epi>
+__device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
+                                     const float* __restrict__ B, int ldb, Epi epi) {
+  Smem* sm = st.sm;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int m0 = 0; m0 < M; m0 += kMT) {
+    for (int n0 = 0; n0 < N; n0 += kNT) {
+      const int nrem = N - n0 < kNT ? N - n0 : kNT;
+      const int NT = (nrem + 15) & ~15;
+      const int nch = (K + kKC - 1) / kKC;
+      const uint32_t idesc = idesc_tf32(NT);
+      for (int c = 0; c < nch; ++c) {
+        const int s = c & 1;
+        wait_stage(st, s);  // MMAs that read this stage (chunk c-2) have completed
+        const int k0 = c * kKC;
+        uint8_t* ah = sm->a[s][0];
+        uint8_t* al = sm->a[s][1];
+        uint8_t* bh = sm->b[s][0];
+        uint8_t* bl = sm->b[s][1];
+        // ---- A chunk: 128 rows x 32 k
+#pragma unroll 4
+        for (int e = tid; e < kMT * kKC; e += kThreads) {
+          int r, k;
+          if (TA) {
+            r = e & (kMT - 1);
+            k = e >> 7;
+          } else {
+            k = e & (kKC - 1);
+            r = e >> 5;
+          }
+          const int gm = m0 + r, gk = k0 + k;
+          float v = 0.f;
+          if (gm < M && gk < K)
+            v = TA ? A[static_cast<size_t>(gk) * lda + gm] : A[static_cast<size_t>(gm) * lda + gk];
+          const float hi = tf32_rn(v);
+          const uint32_t off = sw128_off(r, k);
+          *reinterpret_cast<float*>(ah + off) = hi;
+          if (NPASS > 1) *reinterpret_cast<float*>(al + off) = v - hi;
+        }
+        // ---- B chunk: NT rows (n) x 32 k
+        for (int e = tid; e < NT * kKC; e += kThreads) {
+          int r, k;
+          if (TB) {
+            k = e & (kKC - 1);
+            r = e >> 5;
+          } else {
+            r = e % NT;
+            k = e / NT;
+          }
+          const int gn = n0 + r, gk = k0 + k;
+          float v = 0.f;
+          if (gn < N && gk < K)
+            v = TB ? B[static_cast<size_t>(gn) * ldb + gk] : B[static_cast<size_t>(gk) * ldb + gn];
+          const float hi = tf32_rn(v);
+          const uint32_t off = sw128_off(r, k);
+          *reinterpret_cast<float*>(bh + off) = hi;
+          if (NPASS > 1) *reinterpret_cast<float*>(bl + off) = v - hi;
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+          fence_after();
+          const uint32_t a0 = smem_u32(ah), a1 = smem_u32(al), b0 = smem_u32(bh), b1 = smem_u32(bl);
+#pragma unroll
+          for (int kk = 0; kk < kKC / 8; ++kk) {
+            const uint32_t ko = kk * 32;
+            const uint32_t acc0 = (c > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(st.tmem, kmajor_sw128_desc(a0 + ko), kmajor_sw128_desc(b0 + ko), idesc, acc0);
+            if (NPASS > 1) {
+              mma_tf32(st.tmem, kmajor_sw128_desc(a0 + ko), kmajor_sw128_desc(b1 + ko), idesc, 1u);
+              mma_tf32(st.tmem, kmajor_sw128_desc(a1 + ko), kmajor_sw128_desc(b0 + ko), idesc, 1u);
+            }
+          }
+          mma_commit(&sm->bar[s]);
+        }
+        ++st.uses[s];
+      }
+      // all MMAs of this tile done (commits complete in order)
+      wait_stage(st, 0);
+      wait_stage(st, 1);
+      fence_after();
+      // ---- epilogue: TMEM -> registers -> epi
+      const int q = warp & 3;
+      const int row = m0 + q * 32 + lane;
+      const int half = NT / 2;                     // multiple of 8
+      const int cbeg = (warp < 4) ? 0 : ((half + 15) & ~15);
+      const int cend = (warp < 4) ? ((half + 15) & ~15) : NT;
+      for (int c0 = cbeg; c0 < cend; c0 += 16) {
+        float v[16];
+        tmem_ld16(st.tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), v);
+        if (row < M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = n0 + c0 + j;
+            if (c0 + j < nrem) epi(row, n, v[j]);
+          }
+        }
+      }
+      fence_before();
+      __syncthreads();
+      fence_after();
+    }
+  }
+}
+
+}  // namespace tc
+}  // namespace nb

@@ -36,11 +36,16 @@ def check_rows(ev, rank, n_max, golden_rows):
     return ca
 
 
+PRECS = [nb.PREC_FP32, nb.PREC_TF32, nb.PREC_FP32_SIMT]
+
+
+@pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("case", CASES)
-def test_single_domain_rows_bitexact_and_energy(case):
+def test_single_domain_rows_bitexact_and_energy(case, prec):
+    TOL = nb.TOLERANCE[prec]
     g = load_golden(case)
     m = make_test_model(g)
-    ev = nb.DeviceEvaluator(m, n_ranks=1)
+    ev = nb.DeviceEvaluator(m, n_ranks=1, precision=prec)
     ev.set_debug(True)
     r = ev.compute(g["pos"], g["species"], g["box"])
     ca = check_rows(ev, 0, 64, rows_by_centre(g))
@@ -77,19 +82,21 @@ def test_dd_rows_halo_forces(case, scheme, tag, nr):
     assert rel_err(r["virial"], g["virial"]) <= TOL
 
 
-def test_paper_model_small_system():
+@pytest.mark.parametrize("prec", PRECS)
+def test_paper_model_small_system(prec):
+    TOL = nb.TOLERANCE[prec]
     g = load_golden("paper_small")
     m = nb.init_model(nb.paper_spec(6.0), 1)
-    ev = nb.DeviceEvaluator(m, n_ranks=1)
+    ev = nb.DeviceEvaluator(m, n_ranks=1, precision=prec)
     ev.set_debug(True)
     r = ev.compute(g["pos"], g["species"], g["box"])
     check_rows(ev, 0, 160, rows_by_centre(g))
-    print("paper_small: dE/E", abs(r["energy"] - g["energy"]) / abs(g["energy"]),
+    print("paper_small prec", prec, "dE/E", abs(r["energy"] - g["energy"]) / abs(g["energy"]),
           "dF", rel_err(r["forces"], g["forces"]), "dW", rel_err(r["virial"], g["virial"]))
     assert abs(r["energy"] - g["energy"]) / abs(g["energy"]) <= TOL
     assert rel_err(r["forces"], g["forces"]) <= TOL
     assert rel_err(r["virial"], g["virial"]) <= TOL
-    ev2 = nb.DeviceEvaluator(m, n_ranks=2)
+    ev2 = nb.DeviceEvaluator(m, n_ranks=2, precision=prec)
     r2 = ev2.compute(g["pos"], g["species"], g["box"])
     assert abs(r2["energy"] - g["dd_masked_R2_energy"]) / abs(g["energy"]) <= TOL
     assert rel_err(r2["forces"], g["dd_masked_R2_forces"]) <= TOL
