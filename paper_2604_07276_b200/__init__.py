@@ -38,9 +38,9 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "nnmd_b200.h")
 MASKED_REDUCTION = 0
 WIDE_HALO = 1
 PREC_FP32 = 0        # 3xTF32 tcgen05 (FP32-grade, 1e-5)
-PREC_TF32 = 1        # 1xTF32 tcgen05 (stated tolerance 2e-3)
+PREC_TF32 = 1        # 1xTF32 tcgen05 (stated tolerance 5e-3)
 PREC_FP32_SIMT = 2   # FP32 FMA on CUDA cores (validation path)
-TOLERANCE = {PREC_FP32: 1e-5, PREC_TF32: 2e-3, PREC_FP32_SIMT: 1e-5}
+TOLERANCE = {PREC_FP32: 1e-5, PREC_TF32: 5e-3, PREC_FP32_SIMT: 1e-5}
 
 
 class Error(RuntimeError):

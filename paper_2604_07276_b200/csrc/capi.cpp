@@ -244,16 +244,19 @@ extern "C" nnmd_status nnmd_b200_selftest_gemm(int mode, int ta, int tb, int M, 
                                                const float* B, float* C) {
   return guarded([&] {
     nb::require(M >= 0 && N >= 0 && K >= 0 && mode >= 0 && mode <= 2, "selftest_gemm: bad arguments");
-    const int lda = ta ? M : K, ldb = tb ? K : N;
+    const int ra = ta ? K : M, ca = ta ? M : K, rb = tb ? N : K, cb = tb ? K : N;  // host row-major shapes
+    const int lda = (ca + 3) & ~3, ldb = (cb + 3) & ~3;                         // 16-byte aligned rows
     float *dA = nullptr, *dB = nullptr, *dC = nullptr;
     auto chk = [](cudaError_t e) {
       if (e != cudaSuccess) throw nb::CudaError(std::string("selftest_gemm: ") + cudaGetErrorString(e));
     };
-    chk(cudaMalloc(&dA, sizeof(float) * (static_cast<size_t>(M) * K + 1)));
-    chk(cudaMalloc(&dB, sizeof(float) * (static_cast<size_t>(K) * N + 1)));
+    chk(cudaMalloc(&dA, sizeof(float) * (static_cast<size_t>(ra) * lda + 4)));
+    chk(cudaMalloc(&dB, sizeof(float) * (static_cast<size_t>(rb) * ldb + 4)));
     chk(cudaMalloc(&dC, sizeof(float) * (static_cast<size_t>(M) * N + 1)));
-    chk(cudaMemcpy(dA, A, sizeof(float) * static_cast<size_t>(M) * K, cudaMemcpyHostToDevice));
-    chk(cudaMemcpy(dB, B, sizeof(float) * static_cast<size_t>(K) * N, cudaMemcpyHostToDevice));
+    chk(cudaMemset(dA, 0, sizeof(float) * (static_cast<size_t>(ra) * lda + 4)));
+    chk(cudaMemset(dB, 0, sizeof(float) * (static_cast<size_t>(rb) * ldb + 4)));
+    if (ra && ca) chk(cudaMemcpy2D(dA, lda * sizeof(float), A, ca * sizeof(float), ca * sizeof(float), ra, cudaMemcpyHostToDevice));
+    if (rb && cb) chk(cudaMemcpy2D(dB, ldb * sizeof(float), B, cb * sizeof(float), cb * sizeof(float), rb, cudaMemcpyHostToDevice));
     chk(cudaMemset(dC, 0, sizeof(float) * static_cast<size_t>(M) * N));
     nb::selftest_gemm(mode, ta, tb, M, N, K, dA, lda, dB, ldb, dC);
     chk(cudaGetLastError());

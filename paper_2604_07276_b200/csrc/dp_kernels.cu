@@ -46,14 +46,14 @@ __host__ __device__ inline size_t emb_floats(const DpArgs& a) {
 __host__ __device__ inline size_t align4(size_t x) { return (x + 3) & ~size_t(3); }
 
 __device__ inline Slot slot_of(const DpArgs& a, float* base) {
-  const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a);
+  const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a), nm4 = align4(nm);
   Slot s;
   size_t o = 0;
   s.U = base + o;   o += align4(nm * M2);
-  s.PU = base + o;  o += align4(nm * nm);
-  s.PT = base + o;  o += align4(nm * nm);
-  s.T = base + o;   o += align4(nm * nm);
-  s.Qb = base + o;  o += align4(nm * nm);
+  s.PU = base + o;  o += nm * nm4;
+  s.PT = base + o;  o += nm * nm4;
+  s.T = base + o;   o += nm * nm4;
+  s.Qb = base + o;  o += nm * nm4;
   s.DX0 = base + o; o += align4(nm * W);
   s.DX1 = base + o; o += align4(nm * W);
   s.dU = base + o;  o += align4(nm * M2);
@@ -73,11 +73,11 @@ struct Mm {
   __device__ void finish() {
     if constexpr (MODE != 0) tc::finish(st);
   }
-  template <bool TA, bool TB, class Epi>
+  template <bool TA, bool TB, int PROMOTE = 0, class Epi>
   __device__ __forceinline__ void run(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                                       Epi epi) {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
-    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1>(st, M, N, K, A, lda, B, ldb, epi);
+    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE>(st, M, N, K, A, lda, B, ldb, epi);
   }
 };
 
@@ -188,11 +188,11 @@ __device__ void embed_forward(Mm<MODE>& mm, const DpArgs& a, int n, int zi, cons
 }
 
 // Weighted softmax + gate for every row: PU = pu (optional), PT = s_j^2 pu Theta.
-__device__ void softmax_gate(int n, const float* S, float* PU, float* PT, float inv_sig,
+__device__ void softmax_gate(int n, int ln, const float* S, float* PU, float* PT, float inv_sig,
                              const Smem& sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = wid; k < n; k += nw) {
-    const float* row = S + static_cast<size_t>(k) * n;
+    const float* row = S + static_cast<size_t>(k) * ln;
     float mx = -FLT_MAX;
     for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
     mx = warp_max(mx);
@@ -208,8 +208,8 @@ __device__ void softmax_gate(int n, const float* S, float* PU, float* PT, float 
       const float sj = sm.s[j];
       const float pu = expf(row[j] - mx) * inv;
       const float th = dot4(Rk, sm.R[j]) * inv_sig;
-      if (PU) PU[static_cast<size_t>(k) * n + j] = pu;
-      PT[static_cast<size_t>(k) * n + j] = sj * sj * pu * th;
+      if (PU) PU[static_cast<size_t>(k) * ln + j] = pu;
+      PT[static_cast<size_t>(k) * ln + j] = sj * sj * pu * th;
     }
   }
 }
@@ -218,7 +218,7 @@ __device__ void softmax_gate(int n, const float* S, float* PU, float* PT, float 
 
 size_t dp_scratch_floats(const DpArgs& a) {
   const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a);
-  return align4(nm * M2) * 2 + align4(nm * nm) * 4 + align4(nm * W) * 2 + emb_floats(a) + 64;
+  return align4(nm * M2) * 2 + nm * align4(nm) * 4 + align4(nm * W) * 2 + emb_floats(a) + 64;
 }
 
 size_t dp_smem_bytes(const DpArgs& a, int mode) { return smem_layout(a, mode, nullptr, nullptr) + 1024; }
@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward(const __grid_constant
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
     const int n = a.nn[c];
+    const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     int zi;
     const double sig = centre_rows(a, c, n, sm, zi);
     const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
@@ -252,11 +253,11 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward(const __grid_constant
                           [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
       __syncthreads();
       mm.template run<false, true>(n, n, M, sl.U, M2, Xl, M,
-                         [&](int k, int j, float v) { sl.PU[k * n + j] = v; });
+                         [&](int k, int j, float v) { sl.PU[k * ln + j] = v; });
       __syncthreads();
-      softmax_gate(n, sl.PU, nullptr, sl.PT, inv_sig, sm);
+      softmax_gate(n, ln, sl.PU, nullptr, sl.PT, inv_sig, sm);
       __syncthreads();
-      mm.template run<false, false>(n, M, n, sl.PT, n, sl.U + M, M2,
+      mm.template run<false, false>(n, M, n, sl.PT, ln, sl.U + M, M2,
                           [&](int k, int m, float v) { Xn[k * M + m] = Xl[k * M + m] + v; });
       __syncthreads();
     }
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(256, 1) k_centre_backward(const __grid_constan
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
     const int n = a.nn[c];
+    const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     int zi;
     const double sig = centre_rows(a, c, n, sm, zi);
     const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
@@ -358,20 +360,20 @@ __global__ void __launch_bounds__(256, 1) k_centre_backward(const __grid_constan
                           [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
       __syncthreads();
       mm.template run<false, true>(n, n, M, sl.U, M2, Xl, M,
-                         [&](int k, int j, float v) { sl.PU[k * n + j] = v; });
+                         [&](int k, int j, float v) { sl.PU[k * ln + j] = v; });
       __syncthreads();
-      softmax_gate(n, sl.PU, sl.PU, sl.PT, inv_sig, sm);
+      softmax_gate(n, ln, sl.PU, sl.PU, sl.PT, inv_sig, sm);
       __syncthreads();
       // T = dP~ = dY U_B^T
       mm.template run<false, true>(n, n, M, dY, M, sl.U + M, M2,
-                         [&](int k, int j, float v) { sl.T[k * n + j] = v; });
+                         [&](int k, int j, float v) { sl.T[k * ln + j] = v; });
       __syncthreads();
       // row pass: dP = dP~ Theta, dC = dP~ P / sigma, t_k, dsigma partials
       for (int k = wid; k < n; k += nw) {
         const float4 Rk = sm.R[k];
         float t = 0.f, dsg = 0.f;
         for (int j = lane; j < n; j += 32) {
-          const size_t kj = static_cast<size_t>(k) * n + j;
+          const size_t kj = static_cast<size_t>(k) * ln + j;
           const float sj = sm.s[j];
           const float C = dot4(Rk, sm.R[j]);
           const float dpt = sl.T[kj];
@@ -394,9 +396,9 @@ __global__ void __launch_bounds__(256, 1) k_centre_backward(const __grid_constan
       for (int j = wid; j < n; j += nw) {
         float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
         for (int k = lane; k < n; k += 32) {
-          const size_t kj = static_cast<size_t>(k) * n + j;
+          const size_t kj = static_cast<size_t>(k) * ln + j;
           dw += sl.PU[kj] * (sl.T[kj] - sm.t[k]);
-          const float sym = sl.Qb[kj] + sl.Qb[static_cast<size_t>(j) * n + k];
+          const float sym = sl.Qb[kj] + sl.Qb[static_cast<size_t>(j) * ln + k];
           const float4 Rk = sm.R[k];
           g0 += sym * Rk.x;
           g1 += sym * Rk.y;
@@ -430,18 +432,19 @@ __global__ void __launch_bounds__(256, 1) k_centre_backward(const __grid_constan
       // dS = P o (dP - t)
       for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         const int k = idx / n, j = idx - k * n;
+        const size_t kj = static_cast<size_t>(k) * ln + j;
         const float sj = sm.s[j];
-        sl.T[idx] = sj * sj * sl.PU[idx] * (sl.T[idx] - sm.t[k]);
+        sl.T[kj] = sj * sj * sl.PU[kj] * (sl.T[kj] - sm.t[k]);
       }
       __syncthreads();
       // dU_A = dS X ; dU_B = P~^T dY
-      mm.template run<false, false>(n, M, n, sl.T, n, Xl, M,
+      mm.template run<false, false>(n, M, n, sl.T, ln, Xl, M,
                           [&](int k, int m, float v) { sl.dU[k * M2 + m] = v; });
-      mm.template run<true, false>(n, M, n, sl.PT, n, dY, M,
+      mm.template run<true, false>(n, M, n, sl.PT, ln, dY, M,
                          [&](int k, int m, float v) { sl.dU[k * M2 + M + m] = v; });
       __syncthreads();
       // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T
-      mm.template run<true, false>(n, M, n, sl.T, n, sl.U, M2,
+      mm.template run<true, false>(n, M, n, sl.T, ln, sl.U, M2,
                          [&](int k, int m, float v) { dXn[k * M + m] = dY[k * M + m] + v; });
       __syncthreads();
       mm.template run<false, true>(n, M, M2, sl.dU, M2, AB, M2,
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const 
   const float* Bb = TB ? B + static_cast<size_t>(n0) * ldb : B + n0;
   Mm<MODE> mm;
   mm.init(head);
-  mm.template run<false, TB>(Ms, Ns, K, Ab, K, Bb, ldb, [&](int m, int n, float v) {
+  mm.template run<false, TB, 4>(Ms, Ns, K, Ab, K, Bb, ldb, [&](int m, int n, float v) {
     const size_t o = static_cast<size_t>(m0 + m) * N + n0 + n;
     if (epi_mode == EPI_TANH_BIAS) v = tanhf(v + bias[n0 + n]);
     else if (epi_mode == EPI_DTANH) {

@@ -28,7 +28,8 @@ constexpr int kThreads = 256;
 constexpr int kKC = 32;          // K elements per chunk = one 128-byte swizzle row
 constexpr int kMT = 128;         // MMA M
 constexpr int kNT = 256;         // max MMA N per accumulator tile
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = 512;   // [0,256): MMA partial, [256,512): promoted FP32 sum
+constexpr int kSumCol = 256;
 
 struct alignas(1024) Smem {
   uint8_t a[2][2][kMT * 128];    // [stage][hi/lo]  16 KB each
@@ -122,6 +123,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // Byte offset of element (row, k) of a K-major SW128 tile (rows of 32 fp32).
 __device__ __forceinline__ uint32_t sw128_off(int row, int k) {
   return static_cast<uint32_t>(row * 128 + ((((k >> 2) ^ (row & 7)) & 7) << 4) + ((k & 3) << 2));
@@ -166,12 +179,92 @@ __device__ __forceinline__ void wait_stage(State& st, int s) {
   }
 }
 
-template <bool TA, bool TB, int NPASS, class Epi>
+__device__ __forceinline__ void st_split(uint8_t* hi, uint8_t* lo, uint32_t off, float4 v, bool two) {
+  const float4 h = make_float4(tf32_rn(v.x), tf32_rn(v.y), tf32_rn(v.z), tf32_rn(v.w));
+  *reinterpret_cast<float4*>(hi + off) = h;
+  if (two) *reinterpret_cast<float4*>(lo + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+}
+
+// 4 consecutive elements p[0..3] with per-element guard (count valid = nvalid).
+__device__ __forceinline__ float4 ld4(const float* p, int nvalid) {
+  if (nvalid >= 4) return *reinterpret_cast<const float4*>(p);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (nvalid > 0) v.x = p[0];
+  if (nvalid > 1) v.y = p[1];
+  if (nvalid > 2) v.z = p[2];
+  return v;
+}
+
+// Stage one 32-wide K chunk of an operand with R tile rows (R <= 256, multiple of 16)
+// into K-major SW128 shared memory (hi, and lo when two).  X(r, k) = T ? X[k*ld + r]
+// : X[r*ld + k]; rows >= rows_total and k >= K read as zero.  ld % 4 == 0 and 16-byte
+// aligned base required.  All global loads of the chunk are issued before any store.
+template <bool T>
+__device__ __forceinline__ void stage(const float* __restrict__ X, int ld, int rows_total, int K, int r0, int k0,
+                                      int R, uint8_t* hi, uint8_t* lo, bool two) {
+  const int tid = threadIdx.x;
+  float4 v[8];
+  if (!T) {
+    const int nf = R * 8;  // float4 per chunk
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = tid + i * kThreads;
+      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < nf) {
+        const int r = f >> 3, q = f & 7;
+        const int gr = r0 + r, gk = k0 + 4 * q;
+        if (gr < rows_total && gk < K) v[i] = ld4(X + static_cast<size_t>(gr) * ld + gk, K - gk);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int f = tid + i * kThreads;
+      if (f < nf) st_split(hi, lo, sw128_off(f >> 3, 4 * (f & 7)), v[i], two);
+    }
+  } else {
+    const int rq_n = R >> 2;     // row quads
+    const int nb = rq_n * 8;     // 4x4 blocks
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int b = tid + i * kThreads;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[4 * i + j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (b < nb) {
+        const int rq = b % rq_n, kq = b / rq_n;
+        const int gr = r0 + 4 * rq;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int gk = k0 + 4 * kq + j;
+          if (gk < K && gr < rows_total) v[4 * i + j] = ld4(X + static_cast<size_t>(gk) * ld + gr, rows_total - gr);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int b = tid + i * kThreads;
+      if (b < nb) {
+        const int rq = b % rq_n, kq = b / rq_n;
+        const float4* w = &v[4 * i];
+        st_split(hi, lo, sw128_off(4 * rq + 0, 4 * kq), make_float4(w[0].x, w[1].x, w[2].x, w[3].x), two);
+        st_split(hi, lo, sw128_off(4 * rq + 1, 4 * kq), make_float4(w[0].y, w[1].y, w[2].y, w[3].y), two);
+        st_split(hi, lo, sw128_off(4 * rq + 2, 4 * kq), make_float4(w[0].z, w[1].z, w[2].z, w[3].z), two);
+        st_split(hi, lo, sw128_off(4 * rq + 3, 4 * kq), make_float4(w[0].w, w[1].w, w[2].w, w[3].w), two);
+      }
+    }
+  }
+}
+
+// PROMOTE > 0: every PROMOTE K-chunks the TMEM partial is added (FP32, round-to-nearest)
+// into a second TMEM region and the MMA accumulation restarts.  The tensor core's FP32
+// accumulation truncates (a relative bias growing ~1e-8 per accumulated product); short
+// chains keep long-K products (the K = 4096 fitting layer) at FP32 accuracy.
+template <bool TA, bool TB, int NPASS, int PROMOTE = 0, class Epi>
 __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
                                      const float* __restrict__ B, int ldb, Epi epi) {
   Smem* sm = st.sm;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  constexpr bool two = NPASS > 1;
   for (int m0 = 0; m0 < M; m0 += kMT) {
     for (int n0 = 0; n0 < N; n0 += kNT) {
       const int nrem = N - n0 < kNT ? N - n0 : kNT;
@@ -186,45 +279,8 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
         uint8_t* al = sm->a[s][1];
         uint8_t* bh = sm->b[s][0];
         uint8_t* bl = sm->b[s][1];
-        // ---- A chunk: 128 rows x 32 k
-#pragma unroll 4
-        for (int e = tid; e < kMT * kKC; e += kThreads) {
-          int r, k;
-          if (TA) {
-            r = e & (kMT - 1);
-            k = e >> 7;
-          } else {
-            k = e & (kKC - 1);
-            r = e >> 5;
-          }
-          const int gm = m0 + r, gk = k0 + k;
-          float v = 0.f;
-          if (gm < M && gk < K)
-            v = TA ? A[static_cast<size_t>(gk) * lda + gm] : A[static_cast<size_t>(gm) * lda + gk];
-          const float hi = tf32_rn(v);
-          const uint32_t off = sw128_off(r, k);
-          *reinterpret_cast<float*>(ah + off) = hi;
-          if (NPASS > 1) *reinterpret_cast<float*>(al + off) = v - hi;
-        }
-        // ---- B chunk: NT rows (n) x 32 k
-        for (int e = tid; e < NT * kKC; e += kThreads) {
-          int r, k;
-          if (TB) {
-            k = e & (kKC - 1);
-            r = e >> 5;
-          } else {
-            r = e % NT;
-            k = e / NT;
-          }
-          const int gn = n0 + r, gk = k0 + k;
-          float v = 0.f;
-          if (gn < N && gk < K)
-            v = TB ? B[static_cast<size_t>(gn) * ldb + gk] : B[static_cast<size_t>(gk) * ldb + gn];
-          const float hi = tf32_rn(v);
-          const uint32_t off = sw128_off(r, k);
-          *reinterpret_cast<float*>(bh + off) = hi;
-          if (NPASS > 1) *reinterpret_cast<float*>(bl + off) = v - hi;
-        }
+        stage<TA>(A, lda, M, K, m0, k0, kMT, ah, al, two);
+        stage<!TB>(B, ldb, N, K, n0, k0, NT, bh, bl, two);
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
@@ -233,7 +289,8 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
 #pragma unroll
           for (int kk = 0; kk < kKC / 8; ++kk) {
             const uint32_t ko = kk * 32;
-            const uint32_t acc0 = (c > 0 || kk > 0) ? 1u : 0u;
+            const bool group_start = PROMOTE > 0 ? (c % PROMOTE == 0) : (c == 0);
+            const uint32_t acc0 = (!group_start || kk > 0) ? 1u : 0u;
             mma_tf32(st.tmem, kmajor_sw128_desc(a0 + ko), kmajor_sw128_desc(b0 + ko), idesc, acc0);
             if (NPASS > 1) {
               mma_tf32(st.tmem, kmajor_sw128_desc(a0 + ko), kmajor_sw128_desc(b1 + ko), idesc, 1u);
@@ -243,29 +300,55 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
           mma_commit(&sm->bar[s]);
         }
         ++st.uses[s];
+        if (PROMOTE > 0 && nch > PROMOTE && ((c + 1) % PROMOTE == 0 || c + 1 == nch)) {
+          wait_stage(st, 0);
+          wait_stage(st, 1);
+          fence_after();
+          const bool first = c + 1 <= PROMOTE;
+          const int q = warp & 3;
+          const int half = ((NT >> 1) + 15) & ~15;
+          const int cb = (warp < 4) ? 0 : half, ce = (warp < 4) ? half : NT;
+          const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+          for (int c0 = cb; c0 < ce; c0 += 16) {
+            float p[16], t[16];
+            tmem_ld16(st.tmem + lanes + static_cast<uint32_t>(c0), p);
+            if (!first) {
+              tmem_ld16(st.tmem + lanes + static_cast<uint32_t>(kSumCol + c0), t);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) p[j] += t[j];
+            }
+            tmem_st16(st.tmem + lanes + static_cast<uint32_t>(kSumCol + c0), p);
+          }
+          fence_before();
+          __syncthreads();
+          fence_after();
+        }
       }
       // all MMAs of this tile done (commits complete in order)
       wait_stage(st, 0);
       wait_stage(st, 1);
       fence_after();
-      // ---- epilogue: TMEM -> registers -> epi
+      const uint32_t acc_col = (PROMOTE > 0 && nch > PROMOTE) ? kSumCol : 0u;
+      // ---- epilogue: TMEM -> registers -> shared (row-major, padded) -> coalesced epi
+      float* stg = reinterpret_cast<float*>(sm->a);  // operand stages are free now
+      const int ldst = NT + 4;
       const int q = warp & 3;
-      const int row = m0 + q * 32 + lane;
-      const int half = NT / 2;                     // multiple of 8
-      const int cbeg = (warp < 4) ? 0 : ((half + 15) & ~15);
-      const int cend = (warp < 4) ? ((half + 15) & ~15) : NT;
+      const int half = ((NT >> 1) + 15) & ~15;
+      const int cbeg = (warp < 4) ? 0 : half;
+      const int cend = (warp < 4) ? half : NT;
+      float* srow = stg + static_cast<size_t>(q * 32 + lane) * ldst;
       for (int c0 = cbeg; c0 < cend; c0 += 16) {
         float v[16];
-        tmem_ld16(st.tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), v);
-        if (row < M) {
+        tmem_ld16(st.tmem + (static_cast<uint32_t>(q * 32) << 16) + acc_col + static_cast<uint32_t>(c0), v);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = n0 + c0 + j;
-            if (c0 + j < nrem) epi(row, n, v[j]);
-          }
-        }
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(srow + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
       }
       fence_before();
+      __syncthreads();
+      const int mrows = M - m0 < kMT ? M - m0 : kMT;
+      for (int r = warp; r < mrows; r += kThreads / 32)
+        for (int n = lane; n < nrem; n += 32) epi(m0 + r, n0 + n, stg[static_cast<size_t>(r) * ldst + n]);
       __syncthreads();
       fence_after();
     }

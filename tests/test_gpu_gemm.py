@@ -30,7 +30,7 @@ def run(mode, ta, tb, A, B):
     return Cm
 
 
-@pytest.mark.parametrize("mode,tol", [(0, 2e-6), (1, 2e-6), (2, 2e-3)])
+@pytest.mark.parametrize("mode,tol", [(0, 5e-6), (1, 3e-5), (2, 2e-3)])
 @pytest.mark.parametrize("ta", [0, 1])
 @pytest.mark.parametrize("tb", [0, 1])
 @pytest.mark.parametrize("shape", SHAPES)
