@@ -434,7 +434,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.g = g_.p;
   dp.vir = vir_.p;
   dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
-  const int grid = std::max(1, std::min(ncen, (dp.mode == 0 ? 2 : 1) * n_sm_));
+  const int grid = std::max(1, std::min(ncen, 2 * n_sm_));  // two CTAs per SM (SIMT and tcgen05)
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
   scratch_.ensure(dp.scratch_slot * grid);
   dp.scratch = scratch_.p;

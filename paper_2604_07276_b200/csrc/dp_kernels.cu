@@ -62,13 +62,15 @@ __device__ inline Slot slot_of(const DpArgs& a, float* base) {
 }
 
 // GEMM policy: MODE 0 = SIMT FP32 (gemm_simt.cuh), 1 = 3xTF32 tcgen05, 2 = 1xTF32 tcgen05.
-template <int MODE>
+// NST = tensor-core pipeline stages: 1 for the per-centre kernels (small smem -> two
+// CTAs per SM hide each other's latency), 2 for the fitting-net GEMM tiles.
+template <int MODE, int NST = 1>
 struct Mm {
   GemmSmem* gs;
   tc::State st;
-  __device__ void init(unsigned char* head) {
+  __device__ void init(unsigned char* head, int tmem_cols = 256) {
     if constexpr (MODE == 0) gs = reinterpret_cast<GemmSmem*>(head);
-    else tc::init(st, reinterpret_cast<tc::Smem*>(head));
+    else tc::init(st, reinterpret_cast<tc::Smem<NST>*>(head), tmem_cols);
   }
   __device__ void finish() {
     if constexpr (MODE != 0) tc::finish(st);
@@ -77,12 +79,12 @@ struct Mm {
   __device__ __forceinline__ void run(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                                       Epi epi) {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
-    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE>(st, M, N, K, A, lda, B, ldb, epi);
+    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST>(st, M, N, K, A, lda, B, ldb, epi);
   }
 };
 
-__host__ __device__ inline size_t head_bytes(int mode) {
-  return mode == 0 ? sizeof(GemmSmem) : sizeof(tc::Smem);
+__host__ __device__ inline size_t head_bytes(int mode, int nst = 1) {
+  return mode == 0 ? sizeof(GemmSmem) : (nst == 1 ? sizeof(tc::Smem<1>) : sizeof(tc::Smem<2>));
 }
 
 struct Smem {
@@ -164,7 +166,7 @@ __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int
 // Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
 // Writes intermediate activations to EMB and the last to `out` (n x M).
 template <int MODE>
-__device__ void embed_forward(Mm<MODE>& mm, const DpArgs& a, int n, int zi, const Smem& sm, const Slot& sl,
+__device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, const Smem& sm, const Slot& sl,
                               float* out) {
   const int E0 = a.edims[0];
   float* cur = (a.n_embed == 1) ? out : sl.EMB;
@@ -227,7 +229,7 @@ size_t dp_smem_bytes(const DpArgs& a, int mode) { return smem_layout(a, mode, nu
 // Forward: rows -> embedding -> attention layers -> descriptor D = (X^T R)(R^T X_<) / n_max
 // ------------------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(256, 1) k_centre_forward(const __grid_constant__ DpArgs a) {
+__global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant__ DpArgs a) {
   extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
   Smem sm;
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward(const __grid_constant
 // row gradients g_k = de/dd_k (FP64 geometry), per-centre virial -sum g (x) d.
 // ------------------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(256, 1) k_centre_backward(const __grid_constant__ DpArgs a) {
+__global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constant__ DpArgs a) {
   extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
   Smem sm;
@@ -368,57 +370,70 @@ __global__ void __launch_bounds__(256, 1) k_centre_backward(const __grid_constan
       mm.template run<false, true>(n, n, M, dY, M, sl.U + M, M2,
                          [&](int k, int j, float v) { sl.T[k * ln + j] = v; });
       __syncthreads();
-      // row pass: dP = dP~ Theta, dC = dP~ P / sigma, t_k, dsigma partials
+      // row pass (warp per query row k, coalesced): dP = dP~ Theta, dC = dP~ P / sigma,
+      // t_k = sum_j dP P, dsigma partials, and the row half of the gate term
+      // dR_k += sum_j dC_kj R_j
       for (int k = wid; k < n; k += nw) {
         const float4 Rk = sm.R[k];
-        float t = 0.f, dsg = 0.f;
+        float t = 0.f, dsg = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
         for (int j = lane; j < n; j += 32) {
           const size_t kj = static_cast<size_t>(k) * ln + j;
           const float sj = sm.s[j];
-          const float C = dot4(Rk, sm.R[j]);
+          const float4 Rj = sm.R[j];
+          const float C = dot4(Rk, Rj);
           const float dpt = sl.T[kj];
           const float pv = sj * sj * sl.PU[kj];
           const float dP = dpt * C * inv_sig;
+          const float dC = dpt * pv * inv_sig;
           sl.T[kj] = dP;
-          sl.Qb[kj] = dpt * pv * inv_sig;
-          dsg -= dpt * pv * C * inv_sig * inv_sig;
+          sl.Qb[kj] = dC;
+          dsg -= dC * C * inv_sig;
           t += dP * pv;
+          g0 += dC * Rj.x;
+          g1 += dC * Rj.y;
+          g2 += dC * Rj.z;
+          g3 += dC * Rj.w;
         }
         t = warp_sum(t);
         dsg = warp_sum(dsg);
-        if (lane == 0) {
-          sm.t[k] = t;
-          sm.rowpart[k] = dsg;
-        }
-      }
-      __syncthreads();
-      // column pass: dw_j (softmax weights s_j^2) and the gate's dR_j
-      for (int j = wid; j < n; j += nw) {
-        float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
-        for (int k = lane; k < n; k += 32) {
-          const size_t kj = static_cast<size_t>(k) * ln + j;
-          dw += sl.PU[kj] * (sl.T[kj] - sm.t[k]);
-          const float sym = sl.Qb[kj] + sl.Qb[static_cast<size_t>(j) * ln + k];
-          const float4 Rk = sm.R[k];
-          g0 += sym * Rk.x;
-          g1 += sym * Rk.y;
-          g2 += sym * Rk.z;
-          g3 += sym * Rk.w;
-        }
-        dw = warp_sum(dw);
         g0 = warp_sum(g0);
         g1 = warp_sum(g1);
         g2 = warp_sum(g2);
         g3 = warp_sum(g3);
         if (lane == 0) {
-          sm.dsx[j] += 2.f * sm.s[j] * dw;
-          float4 r = sm.dR[j];
+          sm.t[k] = t;
+          sm.rowpart[k] = dsg;
+          float4 r = sm.dR[k];
           r.x += g0;
           r.y += g1;
           r.z += g2;
           r.w += g3;
-          sm.dR[j] = r;
+          sm.dR[k] = r;
         }
+      }
+      __syncthreads();
+      // column pass (thread per key column j, coalesced across threads): dw_j of the
+      // s_j^2 softmax weights and the column half of the gate term dR_j += sum_k dC_kj R_k
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+#pragma unroll 4
+        for (int k = 0; k < n; ++k) {
+          const size_t kj = static_cast<size_t>(k) * ln + j;
+          dw += sl.PU[kj] * (sl.T[kj] - sm.t[k]);
+          const float dC = sl.Qb[kj];
+          const float4 Rk = sm.R[k];
+          g0 += dC * Rk.x;
+          g1 += dC * Rk.y;
+          g2 += dC * Rk.z;
+          g3 += dC * Rk.w;
+        }
+        sm.dsx[j] += 2.f * sm.s[j] * dw;
+        float4 r = sm.dR[j];
+        r.x += g0;
+        r.y += g1;
+        r.z += g2;
+        r.w += g3;
+        sm.dR[j] = r;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -586,8 +601,8 @@ __global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const 
   const int Ms = min(TM, M - m0), Ns = min(TN, N - n0);
   const float* Ab = A + static_cast<size_t>(m0) * K;
   const float* Bb = TB ? B + static_cast<size_t>(n0) * ldb : B + n0;
-  Mm<MODE> mm;
-  mm.init(head);
+  Mm<MODE, 2> mm;
+  mm.init(head, 512);
   mm.template run<false, TB, 4>(Ms, Ns, K, Ab, K, Bb, ldb, [&](int m, int n, float v) {
     const size_t o = static_cast<size_t>(m0 + m) * N + n0 + n;
     if (epi_mode == EPI_TANH_BIAS) v = tanhf(v + bias[n0 + n]);
@@ -605,7 +620,7 @@ static void fit_gemm(int M, int N, int K, const float* A, const float* B, int ld
                      const float* Y, int epi, cudaStream_t st) {
   constexpr int TM = MODE == 0 ? kTM : tc::kMT;
   constexpr int TN = MODE == 0 ? kTN : tc::kNT;
-  const size_t smem = head_bytes(MODE) + 1024;
+  const size_t smem = head_bytes(MODE, 2) + 1024;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(k_fit_gemm<TB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -693,8 +708,8 @@ __global__ void __launch_bounds__(256, 1) k_selftest_gemm(int M, int N, int K, c
                                                           const float* B, int ldb, float* C) {
   extern __shared__ __align__(1024) unsigned char st_smem_raw[];
   unsigned char* head = st_smem_raw + ((1024 - (tc::smem_u32(st_smem_raw) & 1023)) & 1023);
-  Mm<MODE> mm;
-  mm.init(head);
+  Mm<MODE, 1> mm;
+  mm.init(head, 256);
   mm.template run<TA, TB>(M, N, K, A, lda, B, ldb, [&](int m, int n, float v) { C[static_cast<size_t>(m) * N + n] = v; });
   mm.finish();
 }
@@ -702,7 +717,7 @@ __global__ void __launch_bounds__(256, 1) k_selftest_gemm(int M, int N, int K, c
 template <int MODE>
 static void selftest_mode(int ta, int tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                           float* C) {
-  const size_t smem = head_bytes(MODE) + 1024;
+  const size_t smem = head_bytes(MODE, 1) + 1024;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<1, 256, smem>>>(M, N, K, A, lda, B, ldb, C);

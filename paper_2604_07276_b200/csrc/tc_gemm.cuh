@@ -31,9 +31,12 @@ constexpr int kNT = 256;         // max MMA N per accumulator tile
 constexpr int kTmemCols = 512;   // [0,256): MMA partial, [256,512): promoted FP32 sum
 constexpr int kSumCol = 256;
 
+// Shared-memory image: NST pipeline stages of {A hi, A lo, B hi, B lo}; the epilogue
+// reuses the stage buffers as its staging tile (needs >= 128 x (kNT+4) floats).
+template <int NST>
 struct alignas(1024) Smem {
-  uint8_t a[2][2][kMT * 128];    // [stage][hi/lo]  16 KB each
-  uint8_t b[2][2][kNT * 128];    // [stage][hi/lo]  32 KB each
+  uint8_t a[NST][2][kMT * 128];  // [stage][hi/lo]  16 KB each
+  uint8_t b[NST][2][kNT * 128];  // [stage][hi/lo]  32 KB each
   uint64_t bar[2];
   uint32_t tmem_base;
   uint32_t pad;
@@ -41,7 +44,12 @@ struct alignas(1024) Smem {
 
 // Per-CTA pipeline state (identical in every thread).
 struct State {
-  Smem* sm;
+  uint8_t* a[2][2];
+  uint8_t* b[2][2];
+  uint64_t* bar;
+  uint32_t* tmem_slot;
+  int nst;
+  int cols;             // allocated TMEM columns (256, or 512 with promotion)
   uint32_t tmem;
   uint32_t uses[2];     // commits issued per stage
   uint32_t waited[2];   // commits waited per stage
@@ -141,14 +149,23 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int k) {
 }
 
 // Allocate TMEM and initialise the barriers.  Call once per CTA, all threads.
-__device__ __forceinline__ void init(State& st, Smem* sm) {
-  st.sm = sm;
+template <int NST>
+__device__ __forceinline__ void init(State& st, Smem<NST>* sm, int cols) {
+  for (int s = 0; s < 2; ++s)
+    for (int p = 0; p < 2; ++p) {
+      st.a[s][p] = sm->a[s % NST][p];
+      st.b[s][p] = sm->b[s % NST][p];
+    }
+  st.bar = sm->bar;
+  st.tmem_slot = &sm->tmem_base;
+  st.nst = NST;
+  st.cols = cols;
   st.uses[0] = st.uses[1] = 0;
   st.waited[0] = st.waited[1] = 0;
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm->tmem_base)),
-                 "r"(kTmemCols)
+                 "r"(cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -168,13 +185,13 @@ __device__ __forceinline__ void finish(State& st) {
   __syncthreads();
   fence_after();
   if (threadIdx.x < 32)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(kTmemCols)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(st.tmem), "r"(st.cols)
                  : "memory");
 }
 
 __device__ __forceinline__ void wait_stage(State& st, int s) {
   while (st.waited[s] < st.uses[s]) {
-    mbar_wait(&st.sm->bar[s], st.waited[s] & 1u);
+    mbar_wait(&st.bar[s], st.waited[s] & 1u);
     ++st.waited[s];
   }
 }
@@ -258,10 +275,9 @@ __device__ __forceinline__ void stage(const float* __restrict__ X, int ld, int r
 // into a second TMEM region and the MMA accumulation restarts.  The tensor core's FP32
 // accumulation truncates (a relative bias growing ~1e-8 per accumulated product); short
 // chains keep long-K products (the K = 4096 fitting layer) at FP32 accuracy.
-template <bool TA, bool TB, int NPASS, int PROMOTE = 0, class Epi>
+template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, class Epi>
 __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
                                      const float* __restrict__ B, int ldb, Epi epi) {
-  Smem* sm = st.sm;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   constexpr bool two = NPASS > 1;
@@ -272,13 +288,13 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
       const int nch = (K + kKC - 1) / kKC;
       const uint32_t idesc = idesc_tf32(NT);
       for (int c = 0; c < nch; ++c) {
-        const int s = c & 1;
-        wait_stage(st, s);  // MMAs that read this stage (chunk c-2) have completed
+        const int s = NST == 1 ? 0 : (c & 1);
+        wait_stage(st, s);  // MMAs that read this stage (chunk c-NST) have completed
         const int k0 = c * kKC;
-        uint8_t* ah = sm->a[s][0];
-        uint8_t* al = sm->a[s][1];
-        uint8_t* bh = sm->b[s][0];
-        uint8_t* bl = sm->b[s][1];
+        uint8_t* ah = st.a[s][0];
+        uint8_t* al = st.a[s][1];
+        uint8_t* bh = st.b[s][0];
+        uint8_t* bl = st.b[s][1];
         stage<TA>(A, lda, M, K, m0, k0, kMT, ah, al, two);
         stage<!TB>(B, ldb, N, K, n0, k0, NT, bh, bl, two);
         fence_proxy_async();
@@ -297,7 +313,7 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
               mma_tf32(st.tmem, kmajor_sw128_desc(a1 + ko), kmajor_sw128_desc(b0 + ko), idesc, 1u);
             }
           }
-          mma_commit(&sm->bar[s]);
+          mma_commit(&st.bar[s]);
         }
         ++st.uses[s];
         if (PROMOTE > 0 && nch > PROMOTE && ((c + 1) % PROMOTE == 0 || c + 1 == nch)) {
@@ -329,27 +345,32 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
       wait_stage(st, 1);
       fence_after();
       const uint32_t acc_col = (PROMOTE > 0 && nch > PROMOTE) ? kSumCol : 0u;
-      // ---- epilogue: TMEM -> registers -> shared (row-major, padded) -> coalesced epi
-      float* stg = reinterpret_cast<float*>(sm->a);  // operand stages are free now
-      const int ldst = NT + 4;
+      // ---- epilogue, in column blocks of <= 128: TMEM -> registers -> shared (row-major,
+      // padded) -> coalesced epi over rows
+      float* stg = reinterpret_cast<float*>(st.a[0][0]);  // operand stages are free now
       const int q = warp & 3;
-      const int half = ((NT >> 1) + 15) & ~15;
-      const int cbeg = (warp < 4) ? 0 : half;
-      const int cend = (warp < 4) ? half : NT;
-      float* srow = stg + static_cast<size_t>(q * 32 + lane) * ldst;
-      for (int c0 = cbeg; c0 < cend; c0 += 16) {
-        float v[16];
-        tmem_ld16(st.tmem + (static_cast<uint32_t>(q * 32) << 16) + acc_col + static_cast<uint32_t>(c0), v);
-#pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4*>(srow + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-      }
-      fence_before();
-      __syncthreads();
       const int mrows = M - m0 < kMT ? M - m0 : kMT;
-      for (int r = warp; r < mrows; r += kThreads / 32)
-        for (int n = lane; n < nrem; n += 32) epi(m0 + r, n0 + n, stg[static_cast<size_t>(r) * ldst + n]);
-      __syncthreads();
+      for (int cb0 = 0; cb0 < NT; cb0 += 128) {
+        const int CB = NT - cb0 < 128 ? NT - cb0 : 128;  // multiple of 16
+        const int ldst = CB + 4;
+        const int half = ((CB >> 1) + 15) & ~15;
+        const int cbeg = (warp < 4) ? 0 : half;
+        const int cend = (warp < 4) ? half : CB;
+        float* srow = stg + static_cast<size_t>(q * 32 + lane) * ldst;
+        for (int c0 = cbeg; c0 < cend; c0 += 16) {
+          float v[16];
+          tmem_ld16(st.tmem + (static_cast<uint32_t>(q * 32) << 16) + acc_col + static_cast<uint32_t>(cb0 + c0), v);
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(srow + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+        fence_before();
+        __syncthreads();
+        const int ncols = nrem - cb0 < CB ? nrem - cb0 : CB;
+        for (int r = warp; r < mrows; r += kThreads / 32)
+          for (int n = lane; n < ncols; n += 32) epi(m0 + r, n0 + cb0 + n, stg[static_cast<size_t>(r) * ldst + n]);
+        __syncthreads();
+      }
       fence_after();
     }
   }
