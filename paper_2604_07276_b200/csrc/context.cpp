@@ -17,6 +17,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 namespace nb {
@@ -55,6 +56,7 @@ template struct DevBuf<float>;
 template struct DevBuf<float4>;
 template struct DevBuf<double>;
 template struct DevBuf<int64_t>;
+template struct DevBuf<unsigned long long>;
 
 // partition_ranks (decomp.cpp:17-57): minimise subdomain surface; ties -> most balanced
 // (sorted-descending dims smallest), then lexicographically largest dims.
@@ -425,6 +427,22 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   g_.ensure(static_cast<size_t>(ncen) * nmax * 3 + 3);
   vir_.ensure(static_cast<size_t>(ncen) * 9 + 9);
   e_.ensure(ncen + 1);
+  {
+    const size_t nm4 = (static_cast<size_t>(nmax) + 3) & ~size_t(3);
+    dp.u_layer_stride = static_cast<size_t>(ncen) * nmax * 2 * M;
+    dp.p_layer_stride = static_cast<size_t>(ncen) * nmax * nm4;
+    size_t ew = 0;
+    for (int e = 0; e + 1 < dp.n_embed; ++e) ew += static_cast<size_t>(dp.edims[e]);
+    dp.emb_centre_stride = static_cast<size_t>(nmax) * ew;
+    Ust_.ensure(dp.u_layer_stride * std::max(1, m.na) + 4);
+    PUst_.ensure(dp.p_layer_stride * std::max(1, m.na) + 4);
+    PTst_.ensure(dp.p_layer_stride * std::max(1, m.na) + 4);
+    EMBst_.ensure(dp.emb_centre_stride * ncen + 4);
+    dp.Ust = Ust_.p;
+    dp.PUst = PUst_.p;
+    dp.PTst = PTst_.p;
+    dp.EMBst = EMBst_.p;
+  }
   dp.X = X_.p;
   dp.R = R_.p;
   dp.Ad = Ad_.p;
@@ -473,9 +491,28 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   tic("fit");
   launch_fit(fa, st_);
   toc();
+  static const bool prof_on = getenv("NNMD_PROFILE_PHASES") != nullptr;
+  DevBuf<unsigned long long>* prof = nullptr;
+  if (prof_on) {
+    static DevBuf<unsigned long long> pbuf;
+    pbuf.ensure(24);
+    CU(cudaMemsetAsync(pbuf.p, 0, 24 * sizeof(unsigned long long), st_));
+    dp.prof = pbuf.p;
+    prof = &pbuf;
+  }
   tic("centre_backward");
   launch_centre_backward(dp, grid, st_);
   toc();
+  if (prof) {
+    unsigned long long h[24];
+    CU(cudaMemcpyAsync(h, prof->p, sizeof h, cudaMemcpyDeviceToHost, st_));
+    CU(cudaStreamSynchronize(st_));
+    double tot = 0;
+    for (int i = 0; i < 24; ++i) tot += static_cast<double>(h[i]);
+    fprintf(stderr, "[nnmd phases backward] total %.3e cycles (thread 0 summed over CTAs):", tot);
+    for (int i = 0; i < 16; ++i) fprintf(stderr, " %d:%.1f%%", i, 100.0 * h[i] / (tot > 0 ? tot : 1));
+    fprintf(stderr, "\n");
+  }
   phases_.push_back({rank, 2, ph_in0, timers_.size() - 1});
 
   // ---- forces --------------------------------------------------------------------------

@@ -82,7 +82,7 @@ class Context {
   DevBuf<double> m_pos_;
   DevBuf<int> cell_count_, cell_start_, cell_fill_, cell_members_;
   DevBuf<int> nlist_, nn_, rlist_, rn_;
-  DevBuf<float> X_, Ad_, Bd_, D_, dD_, scratch_, fitY_, fitd_;
+  DevBuf<float> X_, Ad_, Bd_, D_, dD_, scratch_, fitY_, fitd_, Ust_, PUst_, PTst_, EMBst_;
   DevBuf<float4> R_;
   DevBuf<double> g_, vir_, e_, fmem_;
   int* h_counts_ = nullptr;  // pinned

@@ -28,7 +28,7 @@ namespace nb {
 namespace {
 
 struct Slot {
-  float *U, *PU, *PT, *T, *Qb, *DX0, *DX1, *dU, *EMB;
+  float *T, *Qb, *DX0, *DX1, *dU;
 };
 
 __host__ __device__ inline int max_width(const DpArgs& a) {
@@ -49,15 +49,11 @@ __device__ inline Slot slot_of(const DpArgs& a, float* base) {
   const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a), nm4 = align4(nm);
   Slot s;
   size_t o = 0;
-  s.U = base + o;   o += align4(nm * M2);
-  s.PU = base + o;  o += nm * nm4;
-  s.PT = base + o;  o += nm * nm4;
   s.T = base + o;   o += nm * nm4;
   s.Qb = base + o;  o += nm * nm4;
   s.DX0 = base + o; o += align4(nm * W);
   s.DX1 = base + o; o += align4(nm * W);
   s.dU = base + o;  o += align4(nm * M2);
-  s.EMB = base + o;
   return s;
 }
 
@@ -129,6 +125,31 @@ __host__ __device__ inline size_t smem_layout(const DpArgs& a, int mode, unsigne
   return o;
 }
 
+// Phase timer: thread 0 accumulates clock64 deltas per phase id when a.prof is set.
+struct PhaseClock {
+  unsigned long long* out;
+  long long last;
+  unsigned long long acc[24];
+  __device__ void start(unsigned long long* o) {
+    out = o;
+    if (out && threadIdx.x == 0) {
+      last = clock64();
+      for (int i = 0; i < 24; ++i) acc[i] = 0;
+    }
+  }
+  __device__ __forceinline__ void mark(int id) {
+    if (out && threadIdx.x == 0) {
+      const long long t = clock64();
+      acc[id] += static_cast<unsigned long long>(t - last);
+      last = t;
+    }
+  }
+  __device__ void flush() {
+    if (out && threadIdx.x == 0)
+      for (int i = 0; i < 24; ++i) atomicAdd(out + i, acc[i]);
+  }
+};
+
 __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
   return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
 }
@@ -166,10 +187,10 @@ __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int
 // Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
 // Writes intermediate activations to EMB and the last to `out` (n x M).
 template <int MODE>
-__device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, const Smem& sm, const Slot& sl,
+__device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, const Smem& sm, float* emb,
                               float* out) {
   const int E0 = a.edims[0];
-  float* cur = (a.n_embed == 1) ? out : sl.EMB;
+  float* cur = (a.n_embed == 1) ? out : emb;
   for (int idx = threadIdx.x; idx < n * E0; idx += blockDim.x) {
     const int k = idx / E0, o = idx - k * E0;
     const float v = fmaf(sm.s[k], a.w0[o], a.ctab[(static_cast<size_t>(sm.z[k]) * a.ns + zi) * E0 + o]);
@@ -179,7 +200,7 @@ __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, c
   size_t off = static_cast<size_t>(a.n_max) * E0;
   for (int e = 1; e < a.n_embed; ++e) {
     const int Ein = a.edims[e - 1], Eout = a.edims[e];
-    float* nxt = (e + 1 == a.n_embed) ? out : sl.EMB + off;
+    float* nxt = (e + 1 == a.n_embed) ? out : emb + off;
     const float* b = a.eb[e];
     mm.template run<false, true>(n, Eout, Ein, cur, Ein, a.ew[e], Ein,
                        [&](int m, int o, float v) { nxt[m * Eout + o] = tanhf(v + b[o]); });
@@ -220,7 +241,7 @@ __device__ void softmax_gate(int n, int ln, const float* S, float* PU, float* PT
 
 size_t dp_scratch_floats(const DpArgs& a) {
   const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a);
-  return align4(nm * M2) * 2 + nm * align4(nm) * 4 + align4(nm * W) * 2 + emb_floats(a) + 64;
+  return align4(nm * M2) + nm * align4(nm) * 2 + align4(nm * W) * 2 + 64;
 }
 
 size_t dp_smem_bytes(const DpArgs& a, int mode) { return smem_layout(a, mode, nullptr, nullptr) + 1024; }
@@ -247,20 +268,27 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
     float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
     for (int k = threadIdx.x; k < n; k += blockDim.x) Rg[k] = sm.R[k];
     float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
-    embed_forward(mm, a, n, zi, sm, sl, X);
+    embed_forward(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, X);
     for (int l = 0; l < a.n_attn; ++l) {
       const float* Xl = X + l * a.x_layer_stride;
       float* Xn = X + (l + 1) * a.x_layer_stride;
+      float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
+      float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
+      float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
       mm.template run<false, false>(n, M2, M, Xl, M, a.ab[l], M2,
-                          [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
+                          [&](int k, int j, float v) { Ul[k * M2 + j] = v; });
       __syncthreads();
-      mm.template run<false, true>(n, n, M, sl.U, M2, Xl, M,
-                         [&](int k, int j, float v) { sl.PU[k * ln + j] = v; });
+      mm.template run<false, true>(n, n, M, Ul, M2, Xl, M,
+                         [&](int k, int j, float v) { PUl[k * ln + j] = v; });
       __syncthreads();
-      softmax_gate(n, ln, sl.PU, nullptr, sl.PT, inv_sig, sm);
+      softmax_gate(n, ln, PUl, PUl, PTl, inv_sig, sm);
       __syncthreads();
-      mm.template run<false, false>(n, M, n, sl.PT, ln, sl.U + M, M2,
-                          [&](int k, int m, float v) { Xn[k * M + m] = Xl[k * M + m] + v; });
+      {
+        float* __restrict__ xo = Xn;
+        const float* __restrict__ xi = Xl;
+        mm.template run<false, false>(n, M, n, PTl, ln, Ul + M, M2,
+                                      [=](int k, int m, float v) { xo[k * M + m] = xi[k * M + m] + v; });
+      }
       __syncthreads();
     }
     // descriptor (dp_core.hpp:358-384)
@@ -304,6 +332,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   smem_layout(a, MODE, dp_smem, &sm);
   Mm<MODE> mm;
   mm.init(sm.head);
+  PhaseClock pc;
+  pc.start(a.prof);
   const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -312,6 +342,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     int zi;
     const double sig = centre_rows(a, c, n, sm, zi);
+    pc.mark(0);
     const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
     const float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
     const float* Xf = X + a.n_attn * a.x_layer_stride;
@@ -355,21 +386,20 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       reinterpret_cast<float*>(&sm.dR[k])[cc] = v * inm;
     }
     __syncthreads();
+    pc.mark(1);
     for (int l = a.n_attn - 1; l >= 0; --l) {
       const float* Xl = X + l * a.x_layer_stride;
       const float* AB = a.ab[l];
-      mm.template run<false, false>(n, M2, M, Xl, M, AB, M2,
-                          [&](int k, int j, float v) { sl.U[k * M2 + j] = v; });
-      __syncthreads();
-      mm.template run<false, true>(n, n, M, sl.U, M2, Xl, M,
-                         [&](int k, int j, float v) { sl.PU[k * ln + j] = v; });
-      __syncthreads();
-      softmax_gate(n, ln, sl.PU, sl.PU, sl.PT, inv_sig, sm);
-      __syncthreads();
+      // forward stash: U = X [A|B], pu, P~ of this layer (no recompute)
+      const float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
+      const float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
+      const float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
+      pc.mark(2);
       // T = dP~ = dY U_B^T
-      mm.template run<false, true>(n, n, M, dY, M, sl.U + M, M2,
+      mm.template run<false, true>(n, n, M, dY, M, Ul + M, M2,
                          [&](int k, int j, float v) { sl.T[k * ln + j] = v; });
       __syncthreads();
+      pc.mark(5);
       // row pass (warp per query row k, coalesced): dP = dP~ Theta, dC = dP~ P / sigma,
       // t_k = sum_j dP P, dsigma partials, and the row half of the gate term
       // dR_k += sum_j dC_kj R_j
@@ -382,7 +412,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
           const float4 Rj = sm.R[j];
           const float C = dot4(Rk, Rj);
           const float dpt = sl.T[kj];
-          const float pv = sj * sj * sl.PU[kj];
+          const float pv = sj * sj * PUl[kj];
           const float dP = dpt * C * inv_sig;
           const float dC = dpt * pv * inv_sig;
           sl.T[kj] = dP;
@@ -412,6 +442,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         }
       }
       __syncthreads();
+      pc.mark(6);
       // column pass (thread per key column j, coalesced across threads): dw_j of the
       // s_j^2 softmax weights and the column half of the gate term dR_j += sum_k dC_kj R_k
       for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -419,7 +450,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
 #pragma unroll 4
         for (int k = 0; k < n; ++k) {
           const size_t kj = static_cast<size_t>(k) * ln + j;
-          dw += sl.PU[kj] * (sl.T[kj] - sm.t[k]);
+          dw += PUl[kj] * (sl.T[kj] - sm.t[k]);
           const float dC = sl.Qb[kj];
           const float4 Rk = sm.R[k];
           g0 += dC * Rk.x;
@@ -436,6 +467,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         sm.dR[j] = r;
       }
       __syncthreads();
+      pc.mark(7);
+      __syncthreads();
       if (threadIdx.x == 0) {
         float ds = 0.f;
         for (int k = 0; k < n; ++k) ds += sm.rowpart[k];
@@ -449,30 +482,35 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         const int k = idx / n, j = idx - k * n;
         const size_t kj = static_cast<size_t>(k) * ln + j;
         const float sj = sm.s[j];
-        sl.T[kj] = sj * sj * sl.PU[kj] * (sl.T[kj] - sm.t[k]);
+        sl.T[kj] = sj * sj * PUl[kj] * (sl.T[kj] - sm.t[k]);
       }
       __syncthreads();
+      pc.mark(8);
       // dU_A = dS X ; dU_B = P~^T dY
       mm.template run<false, false>(n, M, n, sl.T, ln, Xl, M,
                           [&](int k, int m, float v) { sl.dU[k * M2 + m] = v; });
-      mm.template run<true, false>(n, M, n, sl.PT, ln, dY, M,
+      mm.template run<true, false>(n, M, n, PTl, ln, dY, M,
                          [&](int k, int m, float v) { sl.dU[k * M2 + M + m] = v; });
       __syncthreads();
+      pc.mark(9);
       // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T
-      mm.template run<true, false>(n, M, n, sl.T, ln, sl.U, M2,
-                         [&](int k, int m, float v) { dXn[k * M + m] = dY[k * M + m] + v; });
+      {
+        float* __restrict__ xo = dXn;
+        const float* __restrict__ yi = dY;
+        mm.template run<true, false>(n, M, n, sl.T, ln, Ul, M2,
+                                     [=](int k, int m, float v) { xo[k * M + m] = yi[k * M + m] + v; });
+      }
       __syncthreads();
+      pc.mark(10);
       mm.template run<false, true>(n, M, M2, sl.dU, M2, AB, M2,
                          [&](int k, int m, float v) { dXn[k * M + m] += v; });
       __syncthreads();
+      pc.mark(11);
       float* tmp = dY;
       dY = dXn;
       dXn = tmp;
     }
     // embedding backward (dp_core.hpp:580-596): recompute hidden activations
-    if (a.n_embed > 1) {
-      embed_forward(mm, a, n, zi, sm, sl, dXn);  // last layer output discarded (== X_0)
-    }
     const float* X0 = X;
     for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
       const float y = X0[idx];
@@ -489,7 +527,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
       for (int e = a.n_embed - 1; e >= 1; --e) {
         const int Ein = a.edims[e - 1], Eout = a.edims[e];
-        const float* h = sl.EMB + offs[e - 1];
+        const float* h = a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride + offs[e - 1];
         mm.template run<false, false>(n, Ein, Eout, dY, Eout, a.ew[e], Ein,
                             [&](int k, int i, float v) {
                               const float y = h[k * Ein + i];
@@ -508,6 +546,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
       __syncthreads();
     }
+    pc.mark(12);
     // row gradients (dp_core.hpp:597-611) in FP64 geometry; virial W_ab -= g_a d_b
     {
       const int cm = a.cen_member[c];
@@ -547,7 +586,10 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
     }
     __syncthreads();
-  }  mm.finish();
+    pc.mark(13);
+  }
+  pc.flush();
+  mm.finish();
 }
 
 template <int MODE>

@@ -142,6 +142,14 @@ struct DpArgs {
   // stash (per centre) and scratch (per CTA slot)
   float* X;             // [n_attn+1][n_centres][n_max][M]
   size_t x_layer_stride;
+  // forward stash reused by the backward (no recompute): U = X [A|B] per layer
+  // [n_attn][n_centres][n_max][2M], pu and P~ per layer [n_attn][n_centres][n_max][n_max4],
+  // embedding hidden activations [n_centres][n_max][sum hidden widths]
+  float* Ust;
+  float* PUst;
+  float* PTst;
+  float* EMBst;
+  size_t u_layer_stride, p_layer_stride, emb_centre_stride;
   float4* R;            // [n_centres][n_max]
   float* Ad;            // [n_centres][M*4]
   float* Bd;            // [n_centres][4*mr]
@@ -152,6 +160,7 @@ struct DpArgs {
   float* scratch;
   size_t scratch_slot;  // floats per CTA slot
   int mode;             // 0 SIMT FP32, 1 3xTF32 tcgen05, 2 1xTF32 tcgen05
+  unsigned long long* prof;  // optional per-phase cycle counters (thread 0 of each CTA)
 };
 size_t dp_scratch_floats(const DpArgs& a);
 size_t dp_smem_bytes(const DpArgs& a, int mode);

@@ -212,56 +212,73 @@ __device__ __forceinline__ float4 ld4(const float* p, int nvalid) {
   return v;
 }
 
-// Stage one 32-wide K chunk of an operand with R tile rows (R <= 256, multiple of 16)
-// into K-major SW128 shared memory (hi, and lo when two).  X(r, k) = T ? X[k*ld + r]
-// : X[r*ld + k]; rows >= rows_total and k >= K read as zero.  ld % 4 == 0 and 16-byte
-// aligned base required.  All global loads of the chunk are issued before any store.
-template <bool T>
-__device__ __forceinline__ void stage(const float* __restrict__ X, int ld, int rows_total, int K, int r0, int k0,
-                                      int R, uint8_t* hi, uint8_t* lo, bool two) {
+// One 32-wide K chunk of an operand with R tile rows (R <= 256, multiple of 16), split
+// into a global-load phase (into registers) and a shared-store phase, so the next chunk's
+// loads can be in flight while the tensor core works on the current one.
+// X(r, k) = T ? X[k*ld + r] : X[r*ld + k]; rows >= rows_total and k >= K read as zero;
+// ld % 4 == 0 and a 16-byte aligned base are required.  MAXV float4 per thread:
+// non-transposed R*8/256, transposed 4 * ceil(R*2/256).
+template <int MAXV>
+struct Frag {
+  float4 v[MAXV];
+};
+
+template <bool T, int MAXV>
+__device__ __forceinline__ void load_chunk(const float* __restrict__ X, int ld, int rows_total, int K, int r0,
+                                           int k0, int R, Frag<MAXV>& f) {
   const int tid = threadIdx.x;
-  float4 v[8];
   if (!T) {
-    const int nf = R * 8;  // float4 per chunk
+    const int nf = R * 8;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int f = tid + i * kThreads;
-      v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (f < nf) {
-        const int r = f >> 3, q = f & 7;
+    for (int i = 0; i < MAXV; ++i) {
+      const int e = tid + i * kThreads;
+      f.v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < nf) {
+        const int r = e >> 3, q = e & 7;
         const int gr = r0 + r, gk = k0 + 4 * q;
-        if (gr < rows_total && gk < K) v[i] = ld4(X + static_cast<size_t>(gr) * ld + gk, K - gk);
+        if (gr < rows_total && gk < K) f.v[i] = ld4(X + static_cast<size_t>(gr) * ld + gk, K - gk);
       }
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int f = tid + i * kThreads;
-      if (f < nf) st_split(hi, lo, sw128_off(f >> 3, 4 * (f & 7)), v[i], two);
-    }
   } else {
-    const int rq_n = R >> 2;     // row quads
-    const int nb = rq_n * 8;     // 4x4 blocks
+    const int rq_n = R >> 2;
+    const int nb = rq_n * 8;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < MAXV / 4; ++i) {
       const int b = tid + i * kThreads;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) v[4 * i + j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < 4; ++j) f.v[4 * i + j] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (b < nb) {
         const int rq = b % rq_n, kq = b / rq_n;
         const int gr = r0 + 4 * rq;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int gk = k0 + 4 * kq + j;
-          if (gk < K && gr < rows_total) v[4 * i + j] = ld4(X + static_cast<size_t>(gk) * ld + gr, rows_total - gr);
+          if (gk < K && gr < rows_total) f.v[4 * i + j] = ld4(X + static_cast<size_t>(gk) * ld + gr, rows_total - gr);
         }
       }
     }
+  }
+}
+
+template <bool T, int MAXV>
+__device__ __forceinline__ void store_chunk(int R, const Frag<MAXV>& f, uint8_t* hi, uint8_t* lo, bool two) {
+  const int tid = threadIdx.x;
+  if (!T) {
+    const int nf = R * 8;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < MAXV; ++i) {
+      const int e = tid + i * kThreads;
+      if (e < nf) st_split(hi, lo, sw128_off(e >> 3, 4 * (e & 7)), f.v[i], two);
+    }
+  } else {
+    const int rq_n = R >> 2;
+    const int nb = rq_n * 8;
+#pragma unroll
+    for (int i = 0; i < MAXV / 4; ++i) {
       const int b = tid + i * kThreads;
       if (b < nb) {
         const int rq = b % rq_n, kq = b / rq_n;
-        const float4* w = &v[4 * i];
+        const float4* w = &f.v[4 * i];
         st_split(hi, lo, sw128_off(4 * rq + 0, 4 * kq), make_float4(w[0].x, w[1].x, w[2].x, w[3].x), two);
         st_split(hi, lo, sw128_off(4 * rq + 1, 4 * kq), make_float4(w[0].y, w[1].y, w[2].y, w[3].y), two);
         st_split(hi, lo, sw128_off(4 * rq + 2, 4 * kq), make_float4(w[0].z, w[1].z, w[2].z, w[3].z), two);
@@ -287,16 +304,20 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
       const int NT = (nrem + 15) & ~15;
       const int nch = (K + kKC - 1) / kKC;
       const uint32_t idesc = idesc_tf32(NT);
+      // A: 128 rows -> 4 float4 per thread either way; B: NT <= 256 rows -> <= 8
+      Frag<4> fa;
+      Frag<8> fb;
+      load_chunk<TA, 4>(A, lda, M, K, m0, 0, kMT, fa);
+      load_chunk<!TB, 8>(B, ldb, N, K, n0, 0, NT, fb);
       for (int c = 0; c < nch; ++c) {
         const int s = NST == 1 ? 0 : (c & 1);
         wait_stage(st, s);  // MMAs that read this stage (chunk c-NST) have completed
-        const int k0 = c * kKC;
         uint8_t* ah = st.a[s][0];
         uint8_t* al = st.a[s][1];
         uint8_t* bh = st.b[s][0];
         uint8_t* bl = st.b[s][1];
-        stage<TA>(A, lda, M, K, m0, k0, kMT, ah, al, two);
-        stage<!TB>(B, ldb, N, K, n0, k0, NT, bh, bl, two);
+        store_chunk<TA, 4>(kMT, fa, ah, al, two);
+        store_chunk<!TB, 8>(NT, fb, bh, bl, two);
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
@@ -314,6 +335,10 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
             }
           }
           mma_commit(&st.bar[s]);
+        }
+        if (c + 1 < nch) {  // next chunk's global loads overlap this chunk's MMAs
+          load_chunk<TA, 4>(A, lda, M, K, m0, (c + 1) * kKC, kMT, fa);
+          load_chunk<!TB, 8>(B, ldb, N, K, n0, (c + 1) * kKC, NT, fb);
         }
         ++st.uses[s];
         if (PROMOTE > 0 && nch > PROMOTE && ((c + 1) % PROMOTE == 0 || c + 1 == nch)) {
@@ -367,8 +392,16 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
         fence_before();
         __syncthreads();
         const int ncols = nrem - cb0 < CB ? nrem - cb0 : CB;
-        for (int r = warp; r < mrows; r += kThreads / 32)
-          for (int n = lane; n < ncols; n += 32) epi(m0 + r, n0 + cb0 + n, stg[static_cast<size_t>(r) * ldst + n]);
+        // rows r = warp, warp+8, ...: 4 rows per batch so the functors' global traffic
+        // for independent rows is in flight together
+        for (int r = warp; r < mrows; r += 4 * (kThreads / 32))
+          for (int n = lane; n < ncols; n += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rr = r + u * (kThreads / 32);
+              if (rr < mrows) epi(m0 + rr, n0 + cb0 + n, stg[static_cast<size_t>(rr) * ldst + n]);
+            }
+          }
         __syncthreads();
       }
       fence_after();
