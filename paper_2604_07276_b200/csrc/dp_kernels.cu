@@ -77,6 +77,19 @@ struct Mm {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
     else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST>(st, M, N, K, A, lda, B, ldb, epi);
   }
+  // C = epi(A1 B1 + A2 B2) with one accumulator (tcgen05) or, on the SIMT path, two
+  // passes through `acc` (ld N, must not alias the epilogue's sources).
+  template <bool TA, bool TB, bool TA2, bool TB2, class Epi>
+  __device__ __forceinline__ void run2(int M, int N, int K, const float* A, int lda, const float* B, int ldb, int K2,
+                                       const float* A2, int lda2, const float* B2, int ldb2, float* acc, Epi epi) {
+    if constexpr (MODE == 0) {
+      bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, [&](int m, int n, float v) { acc[m * N + n] = v; });
+      __syncthreads();
+      bgemm<TA2, TB2>(M, N, K2, A2, lda2, B2, ldb2, *gs, [&](int m, int n, float v) { epi(m, n, acc[m * N + n] + v); });
+    } else {
+      tc::gemm2<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 0, NST>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
+    }
+  }
 };
 
 __host__ __device__ inline size_t head_bytes(int mode, int nst = 1) {
@@ -350,20 +363,37 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
     const float* Ad = a.Ad + static_cast<size_t>(c) * M * 4;
     const float* Bd = a.Bd + static_cast<size_t>(c) * 4 * mr;
     // dA[m][cc] = sum_q dD[m,q] B[cc,q];  dB[cc][q] = sum_m dD[m,q] A[m,cc]
-    for (int idx = threadIdx.x; idx < M * 4 + 4 * mr; idx += blockDim.x) {
-      float acc = 0.f;
-      if (idx < M * 4) {
-        const int m = idx >> 2, cc = idx & 3;
-        for (int q = 0; q < mr; ++q) acc += dD[m * mr + q] * Bd[cc * mr + q];
-        sm.dAd[idx] = acc;
-      } else {
-        const int j = idx - M * 4, cc = j / mr, q = j - cc * mr;
-        for (int m = 0; m < M; ++m) acc += dD[m * mr + q] * Ad[m * 4 + cc];
-        sm.dBd[j] = acc;
+    // (operands staged into shared memory with coalesced loads; the tensor-core stage
+    // buffers are idle between GEMMs)
+    {
+      const float* sdD = dD;
+      const float* sAd = Ad;
+      const float* sBd = Bd;
+      if constexpr (MODE != 0) {
+        float* tmp = reinterpret_cast<float*>(sm.head);
+        for (int i = threadIdx.x; i < M * mr; i += blockDim.x) tmp[i] = dD[i];
+        for (int i = threadIdx.x; i < M * 4; i += blockDim.x) tmp[M * mr + i] = Ad[i];
+        for (int i = threadIdx.x; i < 4 * mr; i += blockDim.x) tmp[M * mr + M * 4 + i] = Bd[i];
+        __syncthreads();
+        sdD = tmp;
+        sAd = tmp + M * mr;
+        sBd = tmp + M * mr + M * 4;
       }
+      for (int idx = threadIdx.x; idx < M * 4 + 4 * mr; idx += blockDim.x) {
+        float acc = 0.f;
+        if (idx < M * 4) {
+          const int m = idx >> 2, cc = idx & 3;
+          for (int q = 0; q < mr; ++q) acc += sdD[m * mr + q] * sBd[cc * mr + q];
+          sm.dAd[idx] = acc;
+        } else {
+          const int j = idx - M * 4, cc = j / mr, q = j - cc * mr;
+          for (int m = 0; m < M; ++m) acc += sdD[m * mr + q] * sAd[m * 4 + cc];
+          sm.dBd[j] = acc;
+        }
+      }
+      for (int k = threadIdx.x; k < n; k += blockDim.x) sm.dsx[k] = 0.f;
+      __syncthreads();
     }
-    for (int k = threadIdx.x; k < n; k += blockDim.x) sm.dsx[k] = 0.f;
-    __syncthreads();
     float* dY = sl.DX0;
     float* dXn = sl.DX1;
     const float inm = a.inv_sqrt_nmax;
@@ -378,12 +408,27 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         for (int cc = 0; cc < 4; ++cc) v += sm.dBd[cc * mr + m] * R[cc];
       dY[idx] = v * inm;
     }
-    for (int idx = threadIdx.x; idx < n * 4; idx += blockDim.x) {
-      const int k = idx >> 2, cc = idx & 3;
-      float v = 0.f;
-      for (int m = 0; m < M; ++m) v += Xf[k * M + m] * sm.dAd[m * 4 + cc];
-      for (int q = 0; q < mr; ++q) v += Xf[k * M + q] * sm.dBd[cc * mr + q];
-      reinterpret_cast<float*>(&sm.dR[k])[cc] = v * inm;
+    // dR_k = (X_k dA + X_k[:mr] dB^T) / sqrt(n_max): warp per row, lanes over features
+    for (int k = wid; k < n; k += nw) {
+      float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+      for (int m = lane; m < M; m += 32) {
+        const float x = Xf[k * M + m];
+        v0 += x * sm.dAd[m * 4 + 0];
+        v1 += x * sm.dAd[m * 4 + 1];
+        v2 += x * sm.dAd[m * 4 + 2];
+        v3 += x * sm.dAd[m * 4 + 3];
+        if (m < mr) {
+          v0 += x * sm.dBd[0 * mr + m];
+          v1 += x * sm.dBd[1 * mr + m];
+          v2 += x * sm.dBd[2 * mr + m];
+          v3 += x * sm.dBd[3 * mr + m];
+        }
+      }
+      v0 = warp_sum(v0);
+      v1 = warp_sum(v1);
+      v2 = warp_sum(v2);
+      v3 = warp_sum(v3);
+      if (lane == 0) sm.dR[k] = make_float4(v0 * inm, v1 * inm, v2 * inm, v3 * inm);
     }
     __syncthreads();
     pc.mark(1);
@@ -493,17 +538,13 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
                          [&](int k, int m, float v) { sl.dU[k * M2 + M + m] = v; });
       __syncthreads();
       pc.mark(9);
-      // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T
+      // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T  (both products in one accumulator)
       {
-        float* __restrict__ xo = dXn;
-        const float* __restrict__ yi = dY;
-        mm.template run<true, false>(n, M, n, sl.T, ln, Ul, M2,
-                                     [=](int k, int m, float v) { xo[k * M + m] = yi[k * M + m] + v; });
+        float* xo = dXn;
+        const float* yi = dY;
+        mm.template run2<true, false, false, true>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
+                                                   [=](int k, int m, float v) { xo[k * M + m] = yi[k * M + m] + v; });
       }
-      __syncthreads();
-      pc.mark(10);
-      mm.template run<false, true>(n, M, M2, sl.dU, M2, AB, M2,
-                         [&](int k, int m, float v) { dXn[k * M + m] += v; });
       __syncthreads();
       pc.mark(11);
       float* tmp = dY;

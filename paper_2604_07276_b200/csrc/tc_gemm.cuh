@@ -292,9 +292,12 @@ __device__ __forceinline__ void store_chunk(int R, const Frag<MAXV>& f, uint8_t*
 // into a second TMEM region and the MMA accumulation restarts.  The tensor core's FP32
 // accumulation truncates (a relative bias growing ~1e-8 per accumulated product); short
 // chains keep long-K products (the K = 4096 fitting layer) at FP32 accuracy.
-template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, class Epi>
-__device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
-                                     const float* __restrict__ B, int ldb, Epi epi) {
+// gemm2: C = epi(A1 B1 + A2 B2) accumulated in one TMEM tile (K1 and K2 may differ,
+// K2 = 0 for a single product); one epilogue for both products.
+template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int PROMOTE, int NST, class Epi>
+__device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
+                                      const float* __restrict__ B, int ldb, int K2, const float* __restrict__ A2,
+                                      int lda2, const float* __restrict__ B2, int ldb2, Epi epi) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   constexpr bool two = NPASS > 1;
@@ -302,13 +305,22 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
     for (int n0 = 0; n0 < N; n0 += kNT) {
       const int nrem = N - n0 < kNT ? N - n0 : kNT;
       const int NT = (nrem + 15) & ~15;
-      const int nch = (K + kKC - 1) / kKC;
+      const int nch1 = (K + kKC - 1) / kKC;
+      const int nch = nch1 + (K2 + kKC - 1) / kKC;
       const uint32_t idesc = idesc_tf32(NT);
       // A: 128 rows -> 4 float4 per thread either way; B: NT <= 256 rows -> <= 8
       Frag<4> fa;
       Frag<8> fb;
-      load_chunk<TA, 4>(A, lda, M, K, m0, 0, kMT, fa);
-      load_chunk<!TB, 8>(B, ldb, N, K, n0, 0, NT, fb);
+      auto load = [&](int c) {
+        if (c < nch1) {
+          load_chunk<TA, 4>(A, lda, M, K, m0, c * kKC, kMT, fa);
+          load_chunk<!TB, 8>(B, ldb, N, K, n0, c * kKC, NT, fb);
+        } else {
+          load_chunk<TA2, 4>(A2, lda2, M, K2, m0, (c - nch1) * kKC, kMT, fa);
+          load_chunk<!TB2, 8>(B2, ldb2, N, K2, n0, (c - nch1) * kKC, NT, fb);
+        }
+      };
+      load(0);
       for (int c = 0; c < nch; ++c) {
         const int s = NST == 1 ? 0 : (c & 1);
         wait_stage(st, s);  // MMAs that read this stage (chunk c-NST) have completed
@@ -316,8 +328,13 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
         uint8_t* al = st.a[s][1];
         uint8_t* bh = st.b[s][0];
         uint8_t* bl = st.b[s][1];
-        store_chunk<TA, 4>(kMT, fa, ah, al, two);
-        store_chunk<!TB, 8>(NT, fb, bh, bl, two);
+        if (c < nch1) {
+          store_chunk<TA, 4>(kMT, fa, ah, al, two);
+          store_chunk<!TB, 8>(NT, fb, bh, bl, two);
+        } else {
+          store_chunk<TA2, 4>(kMT, fa, ah, al, two);
+          store_chunk<!TB2, 8>(NT, fb, bh, bl, two);
+        }
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
@@ -336,10 +353,7 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
           }
           mma_commit(&st.bar[s]);
         }
-        if (c + 1 < nch) {  // next chunk's global loads overlap this chunk's MMAs
-          load_chunk<TA, 4>(A, lda, M, K, m0, (c + 1) * kKC, kMT, fa);
-          load_chunk<!TB, 8>(B, ldb, N, K, n0, (c + 1) * kKC, NT, fb);
-        }
+        if (c + 1 < nch) load(c + 1);  // next chunk's global loads overlap this chunk's MMAs
         ++st.uses[s];
         if (PROMOTE > 0 && nch > PROMOTE && ((c + 1) % PROMOTE == 0 || c + 1 == nch)) {
           wait_stage(st, 0);
@@ -407,6 +421,12 @@ __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float
       fence_after();
     }
   }
+}
+
+template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, class Epi>
+__device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
+                                     const float* __restrict__ B, int ldb, Epi epi) {
+  gemm2<TA, TB, TA, TB, NPASS, PROMOTE, NST>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi);
 }
 
 }  // namespace tc
