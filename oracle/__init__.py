@@ -46,7 +46,7 @@ def build(ref: bool = True) -> None:
     """Compile the oracle (port always; the reference only where /root/reference exists)."""
     targets = ["port"]
     if ref and os.path.isdir("/root/reference/proj"):
-        targets.append("ref")
+        targets += ["ref", "integration"]
     subprocess.run(["make", "-s", "-C", HERE, "-j8", *targets], check=True)
 
 
