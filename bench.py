@@ -277,6 +277,11 @@ def run_ours(args, ws, rank, local):
     except Exception:
         pass
     peak = peaks.get("bf16_tflops_sustained", 1366.3)
+    traffic = None
+    try:  # DRAM bytes per launch of the dominant kernel from the latest ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_latest.json")))["k_centre_backward"]["dram_bytes"]
+    except Exception:
+        pass
     achieved = f_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0
 
     # ---- e2e through the host C-ABI entry point (pinned host buffers)
@@ -315,7 +320,7 @@ def run_ours(args, ws, rank, local):
             "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ns_per_day": ns_per_day(e2e)},
             "roofline": {"bound": "tensor", "kernel": "k_centre_backward", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_flop_per_launch": f_bwd, "ms_per_launch": k_bwd,
                          "executed_tflops": npass * x_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0,
                          "mma_passes": npass,

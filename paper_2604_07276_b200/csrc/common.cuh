@@ -74,4 +74,20 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return t;
 }
 
+// ---- scalar / float4 generic helpers for GEMM epilogue functors (called with a float
+// for single elements and a float4 for 4 consecutive, 16-byte aligned columns)
+__device__ __forceinline__ float vld(const float* p, float) { return *p; }
+__device__ __forceinline__ float4 vld(const float* p, float4) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void vst(float* p, float v) { *p = v; }
+__device__ __forceinline__ void vst(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 operator+(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 operator*(float4 a, float4 b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
+__device__ __forceinline__ float vtanh(float a) { return tanhf(a); }
+__device__ __forceinline__ float4 vtanh(float4 a) { return make_float4(tanhf(a.x), tanhf(a.y), tanhf(a.z), tanhf(a.w)); }
+// 1 - y*y (tanh derivative)
+__device__ __forceinline__ float vdtanh(float y) { return 1.f - y * y; }
+__device__ __forceinline__ float4 vdtanh(float4 y) {
+  return make_float4(1.f - y.x * y.x, 1.f - y.y * y.y, 1.f - y.z * y.z, 1.f - y.w * y.w);
+}
+
 }  // namespace nb

@@ -456,9 +456,29 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
   scratch_.ensure(dp.scratch_slot * grid);
   dp.scratch = scratch_.p;
+  static const bool prof_fwd = getenv("NNMD_PROFILE_PHASES") != nullptr;
+  if (prof_fwd) {
+    static DevBuf<unsigned long long> fbuf;
+    fbuf.ensure(24);
+    CU(cudaMemsetAsync(fbuf.p, 0, 24 * sizeof(unsigned long long), st_));
+    dp.prof = fbuf.p;
+  }
   tic("centre_forward");
   launch_centre_forward(dp, grid, st_);
   toc();
+  if (prof_fwd) {
+    unsigned long long h[24];
+    CU(cudaMemcpyAsync(h, dp.prof, sizeof h, cudaMemcpyDeviceToHost, st_));
+    CU(cudaStreamSynchronize(st_));
+    double t0 = 0;
+    for (int i = 0; i < 16; ++i) t0 += static_cast<double>(h[i]);
+    fprintf(stderr, "[nnmd phases forward] total %.3e cycles:", t0);
+    for (int i = 0; i < 8; ++i) fprintf(stderr, " %d:%.1f%%", i, 100.0 * h[i] / (t0 > 0 ? t0 : 1));
+    fprintf(stderr, " | gemm-internal:");
+    for (int i = 16; i < 24; ++i) fprintf(stderr, " g%d:%.1f%%", i - 16, 100.0 * h[i] / (t0 > 0 ? t0 : 1));
+    fprintf(stderr, "\n");
+    dp.prof = nullptr;
+  }
   FitArgs fa{};
   fa.n_fit = dp.n_fit;
   int maxw = 0;
@@ -510,7 +530,11 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     double tot = 0;
     for (int i = 0; i < 24; ++i) tot += static_cast<double>(h[i]);
     fprintf(stderr, "[nnmd phases backward] total %.3e cycles (thread 0 summed over CTAs):", tot);
-    for (int i = 0; i < 16; ++i) fprintf(stderr, " %d:%.1f%%", i, 100.0 * h[i] / (tot > 0 ? tot : 1));
+    double tot0 = 0;
+    for (int i = 0; i < 16; ++i) tot0 += static_cast<double>(h[i]);
+    for (int i = 0; i < 16; ++i) fprintf(stderr, " %d:%.1f%%", i, 100.0 * h[i] / (tot0 > 0 ? tot0 : 1));
+    fprintf(stderr, " | gemm-internal (share of phase total):");
+    for (int i = 16; i < 24; ++i) fprintf(stderr, " g%d:%.1f%%", i - 16, 100.0 * h[i] / (tot0 > 0 ? tot0 : 1));
     fprintf(stderr, "\n");
   }
   phases_.push_back({rank, 2, ph_in0, timers_.size() - 1});

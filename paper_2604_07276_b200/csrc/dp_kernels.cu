@@ -71,11 +71,11 @@ struct Mm {
   __device__ void finish() {
     if constexpr (MODE != 0) tc::finish(st);
   }
-  template <bool TA, bool TB, int PROMOTE = 0, class Epi>
+  template <bool TA, bool TB, int PROMOTE = 0, int EK = 1, class Epi>
   __device__ __forceinline__ void run(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                                       Epi epi) {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
-    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST>(st, M, N, K, A, lda, B, ldb, epi);
+    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
   }
   // C = epi(A1 B1 + A2 B2) with one accumulator (tcgen05) or, on the SIMT path, two
   // passes through `acc` (ld N, must not alias the epilogue's sources).
@@ -87,7 +87,7 @@ struct Mm {
       __syncthreads();
       bgemm<TA2, TB2>(M, N, K2, A2, lda2, B2, ldb2, *gs, [&](int m, int n, float v) { epi(m, n, acc[m * N + n] + v); });
     } else {
-      tc::gemm2<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 0, NST>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
+      tc::gemm2<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 0, NST, 1>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
     }
   }
 };
@@ -216,7 +216,7 @@ __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, c
     float* nxt = (e + 1 == a.n_embed) ? out : emb + off;
     const float* b = a.eb[e];
     mm.template run<false, true>(n, Eout, Ein, cur, Ein, a.ew[e], Ein,
-                       [&](int m, int o, float v) { nxt[m * Eout + o] = tanhf(v + b[o]); });
+                       [&](int m, int o, auto v) { vst(&nxt[m * Eout + o], vtanh(v + vld(&b[o], v))); });
     __syncthreads();
     cur = nxt;
     off += static_cast<size_t>(a.n_max) * Eout;
@@ -224,11 +224,11 @@ __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, c
 }
 
 // Weighted softmax + gate for every row: PU = pu (optional), PT = s_j^2 pu Theta.
-__device__ void softmax_gate(int n, int ln, const float* S, float* PU, float* PT, float inv_sig,
+__device__ void softmax_gate(int n, int ln, const float* S, int lds, float* PU, float* PT, float inv_sig,
                              const Smem& sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = wid; k < n; k += nw) {
-    const float* row = S + static_cast<size_t>(k) * ln;
+    const float* row = S + static_cast<size_t>(k) * lds;
     float mx = -FLT_MAX;
     for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
     mx = warp_max(mx);
@@ -270,6 +270,14 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
   smem_layout(a, MODE, dp_smem, &sm);
   Mm<MODE> mm;
   mm.init(sm.head);
+  PhaseClock pc;
+  pc.start(a.prof);
+  if constexpr (MODE != 0) {
+    if (a.prof && threadIdx.x == 0) {
+      mm.st.prof = pc.acc + 16;
+      mm.st.t_last = clock64();
+    }
+  }
   const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
@@ -277,11 +285,13 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     int zi;
     const double sig = centre_rows(a, c, n, sm, zi);
+    pc.mark(0);
     const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
     float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
     for (int k = threadIdx.x; k < n; k += blockDim.x) Rg[k] = sm.R[k];
     float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
     embed_forward(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, X);
+    pc.mark(1);
     for (int l = 0; l < a.n_attn; ++l) {
       const float* Xl = X + l * a.x_layer_stride;
       float* Xn = X + (l + 1) * a.x_layer_stride;
@@ -289,20 +299,38 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
       float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
       float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
       mm.template run<false, false>(n, M2, M, Xl, M, a.ab[l], M2,
-                          [&](int k, int j, float v) { Ul[k * M2 + j] = v; });
+                          [&](int k, int j, auto v) { vst(&Ul[k * M2 + j], v); });
       __syncthreads();
-      mm.template run<false, true>(n, n, M, Ul, M2, Xl, M,
-                         [&](int k, int j, float v) { PUl[k * ln + j] = v; });
+      pc.mark(2);
+      bool fused_softmax = false;
+      if constexpr (MODE != 0) {
+        if (n <= 128) {
+          // S tile stays in shared memory: weighted softmax + gate fused into the epilogue
+          mm.template run<false, true, 0, 2>(n, n, M, Ul, M2, Xl, M,
+                                             [&](const float* stg, int ldst, int, int, int, int) {
+                                               softmax_gate(n, ln, stg, ldst, PUl, PTl, inv_sig, sm);
+                                             });
+          pc.mark(3);
+          fused_softmax = true;
+        }
+      }
+      if (!fused_softmax) {
+        mm.template run<false, true>(n, n, M, Ul, M2, Xl, M,
+                                     [&](int k, int j, auto v) { vst(&PUl[k * ln + j], v); });
+        __syncthreads();
+        pc.mark(3);
+        softmax_gate(n, ln, PUl, ln, PUl, PTl, inv_sig, sm);
+      }
       __syncthreads();
-      softmax_gate(n, ln, PUl, PUl, PTl, inv_sig, sm);
-      __syncthreads();
+      pc.mark(4);
       {
         float* __restrict__ xo = Xn;
         const float* __restrict__ xi = Xl;
         mm.template run<false, false>(n, M, n, PTl, ln, Ul + M, M2,
-                                      [=](int k, int m, float v) { xo[k * M + m] = xi[k * M + m] + v; });
+                                      [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&xi[k * M + m], v) + v); });
       }
       __syncthreads();
+      pc.mark(5);
     }
     // descriptor (dp_core.hpp:358-384)
     const float* Xf = X + a.n_attn * a.x_layer_stride;
@@ -330,7 +358,10 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
     for (int idx = threadIdx.x; idx < M * 4; idx += blockDim.x) a.Ad[static_cast<size_t>(c) * M * 4 + idx] = sm.Ad[idx];
     for (int idx = threadIdx.x; idx < 4 * mr; idx += blockDim.x) a.Bd[static_cast<size_t>(c) * 4 * mr + idx] = sm.Bd[idx];
     __syncthreads();
-  }  mm.finish();
+    pc.mark(6);
+  }
+  pc.flush();
+  mm.finish();
 }
 
 // ------------------------------------------------------------------------------------
@@ -347,6 +378,12 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   mm.init(sm.head);
   PhaseClock pc;
   pc.start(a.prof);
+  if constexpr (MODE != 0) {
+    if (a.prof && threadIdx.x == 0) {
+      mm.st.prof = pc.acc + 16;
+      mm.st.t_last = clock64();
+    }
+  }
   const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -442,7 +479,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       pc.mark(2);
       // T = dP~ = dY U_B^T
       mm.template run<false, true>(n, n, M, dY, M, Ul + M, M2,
-                         [&](int k, int j, float v) { sl.T[k * ln + j] = v; });
+                         [&](int k, int j, auto v) { vst(&sl.T[k * ln + j], v); });
       __syncthreads();
       pc.mark(5);
       // row pass (warp per query row k, coalesced): dP = dP~ Theta, dC = dP~ P / sigma,
@@ -533,9 +570,9 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       pc.mark(8);
       // dU_A = dS X ; dU_B = P~^T dY
       mm.template run<false, false>(n, M, n, sl.T, ln, Xl, M,
-                          [&](int k, int m, float v) { sl.dU[k * M2 + m] = v; });
+                          [&](int k, int m, auto v) { vst(&sl.dU[k * M2 + m], v); });
       mm.template run<true, false>(n, M, n, PTl, ln, dY, M,
-                         [&](int k, int m, float v) { sl.dU[k * M2 + M + m] = v; });
+                         [&](int k, int m, auto v) { vst(&sl.dU[k * M2 + M + m], v); });
       __syncthreads();
       pc.mark(9);
       // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T  (both products in one accumulator)
@@ -543,7 +580,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         float* xo = dXn;
         const float* yi = dY;
         mm.template run2<true, false, false, true>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
-                                                   [=](int k, int m, float v) { xo[k * M + m] = yi[k * M + m] + v; });
+                                                   [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&yi[k * M + m], v) + v); });
       }
       __syncthreads();
       pc.mark(11);
@@ -570,9 +607,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         const int Ein = a.edims[e - 1], Eout = a.edims[e];
         const float* h = a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride + offs[e - 1];
         mm.template run<false, false>(n, Ein, Eout, dY, Eout, a.ew[e], Ein,
-                            [&](int k, int i, float v) {
-                              const float y = h[k * Ein + i];
-                              dXn[k * Ein + i] = v * (1.f - y * y);
+                            [&](int k, int i, auto v) {
+                              vst(&dXn[k * Ein + i], v * vdtanh(vld(&h[k * Ein + i], v)));
                             });
         __syncthreads();
         float* tmp = dY;
@@ -686,14 +722,11 @@ __global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const 
   const float* Bb = TB ? B + static_cast<size_t>(n0) * ldb : B + n0;
   Mm<MODE, 2> mm;
   mm.init(head, 512);
-  mm.template run<false, TB, 4>(Ms, Ns, K, Ab, K, Bb, ldb, [&](int m, int n, float v) {
+  mm.template run<false, TB, 4>(Ms, Ns, K, Ab, K, Bb, ldb, [&](int m, int n, auto v) {
     const size_t o = static_cast<size_t>(m0 + m) * N + n0 + n;
-    if (epi_mode == EPI_TANH_BIAS) v = tanhf(v + bias[n0 + n]);
-    else if (epi_mode == EPI_DTANH) {
-      const float y = Y[o];
-      v *= 1.f - y * y;
-    }
-    C[o] = v;
+    if (epi_mode == EPI_TANH_BIAS) v = vtanh(v + vld(&bias[n0 + n], v));
+    else if (epi_mode == EPI_DTANH) v = v * vdtanh(vld(&Y[o], v));
+    vst(&C[o], v);
   });
   mm.finish();
 }
@@ -793,7 +826,7 @@ __global__ void __launch_bounds__(256, 1) k_selftest_gemm(int M, int N, int K, c
   unsigned char* head = st_smem_raw + ((1024 - (tc::smem_u32(st_smem_raw) & 1023)) & 1023);
   Mm<MODE, 1> mm;
   mm.init(head, 256);
-  mm.template run<TA, TB>(M, N, K, A, lda, B, ldb, [&](int m, int n, float v) { C[static_cast<size_t>(m) * N + n] = v; });
+  mm.template run<TA, TB, 0, 0>(M, N, K, A, lda, B, ldb, [&](int m, int n, float v) { C[static_cast<size_t>(m) * N + n] = v; });
   mm.finish();
 }
 

@@ -53,6 +53,15 @@ struct State {
   uint32_t tmem;
   uint32_t uses[2];     // commits issued per stage
   uint32_t waited[2];   // commits waited per stage
+  unsigned long long* prof;  // optional: thread 0 accumulates cycles per GEMM stage (ids 0..7)
+  long long t_last;
+  __device__ __forceinline__ void tick(int id) {
+    if (prof && threadIdx.x == 0) {
+      const long long t = clock64();
+      if (id >= 0) prof[id] += static_cast<unsigned long long>(t - t_last);
+      t_last = t;
+    }
+  }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -162,6 +171,8 @@ __device__ __forceinline__ void init(State& st, Smem<NST>* sm, int cols) {
   st.cols = cols;
   st.uses[0] = st.uses[1] = 0;
   st.waited[0] = st.waited[1] = 0;
+  st.prof = nullptr;
+  st.t_last = 0;
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm->tmem_base)),
@@ -294,7 +305,11 @@ __device__ __forceinline__ void store_chunk(int R, const Frag<MAXV>& f, uint8_t*
 // chains keep long-K products (the K = 4096 fitting layer) at FP32 accuracy.
 // gemm2: C = epi(A1 B1 + A2 B2) accumulated in one TMEM tile (K1 and K2 may differ,
 // K2 = 0 for a single product); one epilogue for both products.
-template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int PROMOTE, int NST, class Epi>
+// EK = epilogue kind: 0 scalar functor epi(m, n, float); 1 vector functor (also called
+// with float4 for 4 consecutive aligned columns); 2 tile functor, called once per column
+// block by all threads with the SMEM-staged accumulator tile:
+// epi(const float* stg, int ldst, int mrows, int ncols, int m_base, int n_base).
+template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int PROMOTE, int NST, int EK = 1, class Epi>
 __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
                                       const float* __restrict__ B, int ldb, int K2, const float* __restrict__ A2,
                                       int lda2, const float* __restrict__ B2, int ldb2, Epi epi) {
@@ -320,10 +335,13 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
           load_chunk<!TB2, 8>(B2, ldb2, N, K2, n0, (c - nch1) * kKC, NT, fb);
         }
       };
+      st.tick(-1);
       load(0);
+      st.tick(0);
       for (int c = 0; c < nch; ++c) {
         const int s = NST == 1 ? 0 : (c & 1);
         wait_stage(st, s);  // MMAs that read this stage (chunk c-NST) have completed
+        st.tick(1);
         uint8_t* ah = st.a[s][0];
         uint8_t* al = st.a[s][1];
         uint8_t* bh = st.b[s][0];
@@ -335,8 +353,10 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
           store_chunk<TA2, 4>(kMT, fa, ah, al, two);
           store_chunk<!TB2, 8>(NT, fb, bh, bl, two);
         }
+        st.tick(2);
         fence_proxy_async();
         __syncthreads();
+        st.tick(3);
         if (tid == 0) {
           fence_after();
           const uint32_t a0 = smem_u32(ah), a1 = smem_u32(al), b0 = smem_u32(bh), b1 = smem_u32(bl);
@@ -353,7 +373,9 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
           }
           mma_commit(&st.bar[s]);
         }
+        st.tick(4);
         if (c + 1 < nch) load(c + 1);  // next chunk's global loads overlap this chunk's MMAs
+        st.tick(0);
         ++st.uses[s];
         if (PROMOTE > 0 && nch > PROMOTE && ((c + 1) % PROMOTE == 0 || c + 1 == nch)) {
           wait_stage(st, 0);
@@ -383,6 +405,7 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
       wait_stage(st, 0);
       wait_stage(st, 1);
       fence_after();
+      st.tick(5);
       const uint32_t acc_col = (PROMOTE > 0 && nch > PROMOTE) ? kSumCol : 0u;
       // ---- epilogue, in column blocks of <= 128: TMEM -> registers -> shared (row-major,
       // padded) -> coalesced epi over rows
@@ -405,28 +428,48 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
         }
         fence_before();
         __syncthreads();
+        st.tick(6);
         const int ncols = nrem - cb0 < CB ? nrem - cb0 : CB;
-        // rows r = warp, warp+8, ...: 4 rows per batch so the functors' global traffic
-        // for independent rows is in flight together
-        for (int r = warp; r < mrows; r += 4 * (kThreads / 32))
-          for (int n = lane; n < ncols; n += 32) {
+        if constexpr (EK == 2) {
+          epi(stg, ldst, mrows, ncols, m0, n0 + cb0);
+        } else if constexpr (EK == 1) {
+          // float4 per thread, rows r = warp, warp+8, ... four rows per batch in flight
+          const int nq = ncols >> 2;
+          for (int r = warp; r < mrows; r += 4 * (kThreads / 32))
+            for (int qd = lane; qd < nq; qd += 32) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int rr = r + u * (kThreads / 32);
-              if (rr < mrows) epi(m0 + rr, n0 + cb0 + n, stg[static_cast<size_t>(rr) * ldst + n]);
+              for (int u = 0; u < 4; ++u) {
+                const int rr = r + u * (kThreads / 32);
+                if (rr < mrows)
+                  epi(m0 + rr, n0 + cb0 + 4 * qd, *reinterpret_cast<const float4*>(stg + static_cast<size_t>(rr) * ldst + 4 * qd));
+              }
             }
+          for (int e = threadIdx.x; e < mrows * (ncols - 4 * nq); e += kThreads) {
+            const int rr = e / (ncols - 4 * nq), cc = 4 * nq + e % (ncols - 4 * nq);
+            epi(m0 + rr, n0 + cb0 + cc, stg[static_cast<size_t>(rr) * ldst + cc]);
           }
+        } else {
+          for (int r = warp; r < mrows; r += 4 * (kThreads / 32))
+            for (int n = lane; n < ncols; n += 32) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int rr = r + u * (kThreads / 32);
+                if (rr < mrows) epi(m0 + rr, n0 + cb0 + n, stg[static_cast<size_t>(rr) * ldst + n]);
+              }
+            }
+        }
         __syncthreads();
+        st.tick(7);
       }
       fence_after();
     }
   }
 }
 
-template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, class Epi>
+template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, int EK = 1, class Epi>
 __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
                                      const float* __restrict__ B, int ldb, Epi epi) {
-  gemm2<TA, TB, TA, TB, NPASS, PROMOTE, NST>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi);
+  gemm2<TA, TB, TA, TB, NPASS, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi);
 }
 
 }  // namespace tc
