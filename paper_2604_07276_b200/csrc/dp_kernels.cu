@@ -77,6 +77,13 @@ struct Mm {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
     else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
   }
+  // Small GEMMs (the embedding net, N <= 128, K <= 128): the SIMT block GEMM on the idle
+  // tensor-core stage buffer beats tensor-core staging/epilogue latency at these sizes.
+  template <bool TA, bool TB, class Epi>
+  __device__ __forceinline__ void run_small(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                                            unsigned char* head, Epi epi) {
+    bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *reinterpret_cast<GemmSmem*>(head), epi);
+  }
   // C = epi(A1 B1 + A2 B2) with one accumulator (tcgen05) or, on the SIMT path, two
   // passes through `acc` (ld N, must not alias the epilogue's sources).
   template <bool TA, bool TB, bool TA2, bool TB2, class Epi>
@@ -216,7 +223,7 @@ __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, c
     float* nxt = (e + 1 == a.n_embed) ? out : emb + off;
     const float* b = a.eb[e];
     mm.template run<false, true>(n, Eout, Ein, cur, Ein, a.ew[e], Ein,
-                       [&](int m, int o, auto v) { vst(&nxt[m * Eout + o], vtanh(v + vld(&b[o], v))); });
+                                 [&](int m, int o, auto v) { vst(&nxt[m * Eout + o], vtanh(v + vld(&b[o], v))); });
     __syncthreads();
     cur = nxt;
     off += static_cast<size_t>(a.n_max) * Eout;
@@ -227,8 +234,41 @@ __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, c
 __device__ void softmax_gate(int n, int ln, const float* S, int lds, float* PU, float* PT, float inv_sig,
                              const Smem& sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  constexpr int kMaxC = 8;  // register-cached row chunks: n <= 256
   for (int k = wid; k < n; k += nw) {
     const float* row = S + static_cast<size_t>(k) * lds;
+    if (n <= 32 * kMaxC) {
+      float e[kMaxC];
+      float mx = -FLT_MAX;
+#pragma unroll
+      for (int t = 0; t < kMaxC; ++t) {
+        const int j = lane + 32 * t;
+        e[t] = j < n ? row[j] : -FLT_MAX;
+        mx = fmaxf(mx, e[t]);
+      }
+      mx = warp_max(mx);
+      float den = 0.f;
+#pragma unroll
+      for (int t = 0; t < kMaxC; ++t) {
+        const int j = lane + 32 * t;
+        e[t] = j < n ? expf(e[t] - mx) : 0.f;
+        if (j < n) den += sm.s[j] * sm.s[j] * e[t];
+      }
+      den = warp_sum(den);
+      const float inv = den > 0.f ? 1.0f / den : 0.f;
+      const float4 Rk = sm.R[k];
+#pragma unroll
+      for (int t = 0; t < kMaxC; ++t) {
+        const int j = lane + 32 * t;
+        if (j < n) {
+          const float sj = sm.s[j];
+          const float pu = e[t] * inv;
+          if (PU) PU[static_cast<size_t>(k) * ln + j] = pu;
+          PT[static_cast<size_t>(k) * ln + j] = sj * sj * pu * (dot4(Rk, sm.R[j]) * inv_sig);
+        }
+      }
+      continue;
+    }
     float mx = -FLT_MAX;
     for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
     mx = warp_max(mx);
@@ -525,40 +565,53 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
       __syncthreads();
       pc.mark(6);
-      // column pass (thread per key column j, coalesced across threads): dw_j of the
-      // s_j^2 softmax weights and the column half of the gate term dR_j += sum_k dC_kj R_k
-      for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+      // column pass (thread per key column j and k-half, coalesced across threads): dw_j
+      // of the s_j^2 softmax weights and the column half of the gate term
+      // dR_j += sum_k dC_kj R_k.  Two k-halves per column double the active threads.
+      {
+        const int nh = (n + 1) >> 1;
+        const int half_threads = blockDim.x >> 1;
+        float4* part = reinterpret_cast<float4*>(sm.head);          // [2][n] (g0..g3)
+        float* partw = reinterpret_cast<float*>(part + 2 * a.n_max);   // [2][n]
+        const int h = threadIdx.x / half_threads;
+        for (int j = threadIdx.x - h * half_threads; j < n; j += half_threads) {
+          float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+          const int kb = h * nh, ke = min(n, kb + nh);
 #pragma unroll 4
-        for (int k = 0; k < n; ++k) {
-          const size_t kj = static_cast<size_t>(k) * ln + j;
-          dw += PUl[kj] * (sl.T[kj] - sm.t[k]);
-          const float dC = sl.Qb[kj];
-          const float4 Rk = sm.R[k];
-          g0 += dC * Rk.x;
-          g1 += dC * Rk.y;
-          g2 += dC * Rk.z;
-          g3 += dC * Rk.w;
+          for (int k = kb; k < ke; ++k) {
+            const size_t kj = static_cast<size_t>(k) * ln + j;
+            dw += PUl[kj] * (sl.T[kj] - sm.t[k]);
+            const float dC = sl.Qb[kj];
+            const float4 Rk = sm.R[k];
+            g0 += dC * Rk.x;
+            g1 += dC * Rk.y;
+            g2 += dC * Rk.z;
+            g3 += dC * Rk.w;
+          }
+          part[h * a.n_max + j] = make_float4(g0, g1, g2, g3);
+          partw[h * a.n_max + j] = dw;
         }
-        sm.dsx[j] += 2.f * sm.s[j] * dw;
-        float4 r = sm.dR[j];
-        r.x += g0;
-        r.y += g1;
-        r.z += g2;
-        r.w += g3;
-        sm.dR[j] = r;
+        if (threadIdx.x == blockDim.x - 1) {
+          float ds = 0.f;
+          for (int k = 0; k < n; ++k) ds += sm.rowpart[k];
+          sm.red[0] = ds;
+        }
+        __syncthreads();
+        const float dsig = static_cast<float>(sm.red[0]);
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+          const float4 p0 = part[j], p1 = part[a.n_max + j];
+          const float dw = partw[j] + partw[a.n_max + j];
+          sm.dsx[j] += 2.f * sm.s[j] * (dw + dsig);
+          float4 r = sm.dR[j];
+          r.x += p0.x + p1.x;
+          r.y += p0.y + p1.y;
+          r.z += p0.z + p1.z;
+          r.w += p0.w + p1.w;
+          sm.dR[j] = r;
+        }
       }
       __syncthreads();
       pc.mark(7);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        float ds = 0.f;
-        for (int k = 0; k < n; ++k) ds += sm.rowpart[k];
-        sm.red[0] = ds;
-      }
-      __syncthreads();
-      const float dsig = static_cast<float>(sm.red[0]);
-      for (int k = threadIdx.x; k < n; k += blockDim.x) sm.dsx[k] += 2.f * sm.s[k] * dsig;
       // dS = P o (dP - t)
       for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
         const int k = idx / n, j = idx - k * n;
