@@ -111,12 +111,20 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   require(o.n_ranks <= 48, "nnmd_b200: at most 48 DD ranks");
   stats_.resize(static_cast<size_t>(o.n_ranks));
   debug_.resize(static_cast<size_t>(o.n_ranks));
-  if (o.world_size > 1) {
+  // NNMD_FORCE_NCCL=1 creates the communicator even for one process (exercises the NCCL
+  // path -- dlopen, ncclCommInitRank, ncclAllReduce -- on a single GPU).
+  use_nccl_ = o.world_size > 1 || getenv("NNMD_FORCE_NCCL") != nullptr;
+  if (use_nccl_) {
     const Nccl& N = nccl();
     require(N.ok, "nnmd_b200: NCCL unavailable: " + N.err);
-    require(o.nccl_id != nullptr, "nnmd_b200: world_size > 1 needs an nccl_id");
     NcclUid uid;
-    std::memcpy(&uid, o.nccl_id, sizeof uid);
+    if (o.nccl_id) {
+      std::memcpy(&uid, o.nccl_id, sizeof uid);
+    } else {
+      require(o.world_size == 1, "nnmd_b200: world_size > 1 needs an nccl_id");
+      const int r0 = N.GetUniqueId(&uid);
+      if (r0 != 0) throw CudaError(std::string("ncclGetUniqueId: ") + N.GetErrorString(r0));
+    }
     const int r = N.CommInitRank(&comm_, o.world_size, uid, o.world_rank);
     if (r != 0) throw CudaError(std::string("ncclCommInitRank: ") + N.GetErrorString(r));
   }
@@ -205,7 +213,7 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   toc();
   for (int r = 0; r < opts_.n_ranks; ++r)
     if (r % opts_.world_size == opts_.world_rank) run_rank(r, sys, dims.data(), thickness, d_out, keep_debug_);
-  if (opts_.world_size > 1) {
+  if (use_nccl_) {
     tic("nccl_allreduce");
     const Nccl& N = nccl();
     const int rc = N.AllReduce(d_out, d_out, out_len, kNcclFloat64, kNcclSum, comm_, st_);
@@ -218,7 +226,7 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   if (opts_.scheme == NNMD_MASKED_REDUCTION)
     for (int r = 0; r < opts_.n_ranks; ++r)
       if (r % opts_.world_size == opts_.world_rank) stats_[static_cast<size_t>(r)].counts[3] = h_counts_[16 + (r % 48)];
-  if (opts_.world_size > 1) {
+  if (use_nccl_) {
     const double comm = ktimes_.back().second;
     for (auto& s : stats_) s.ms[3] += comm;
   }

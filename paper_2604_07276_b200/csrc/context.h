@@ -68,6 +68,7 @@ class Context {
   int n_sm_ = 148;
   DevBuf<float> weights_;
   NcclComm comm_ = nullptr;
+  bool use_nccl_ = false;
 
   // inputs (host-API path) and outputs
   DevBuf<double> pos_, out_;

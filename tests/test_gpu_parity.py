@@ -199,3 +199,17 @@ def test_full_size_1hci_properties():
         e, _ = port.evaluate_center(h, int(sp[c]), d[rows], sp[mem[rows]])
         assert abs(r1["atom_energy"][c] - e) <= TOL * max(abs(e), 1e-3)
     port.model_free(h)
+
+
+def test_nccl_collective_path_single_gpu(monkeypatch):
+    """The NCCL collective-2 path (dlopen libnccl, ncclCommInitRank, in-place f64
+    ncclAllReduce of [E, W, F, e_i]) on one GPU gives the same result as without it."""
+    g = load_golden("dd_case_1")
+    m = make_test_model(g)
+    r0 = nb.DeviceEvaluator(m, n_ranks=2).compute(g["pos"], g["species"], g["box"])
+    monkeypatch.setenv("NNMD_FORCE_NCCL", "1")
+    ev = nb.DeviceEvaluator(m, n_ranks=2)
+    r1 = ev.compute(g["pos"], g["species"], g["box"])
+    assert r1["energy"] == r0["energy"]
+    assert np.array_equal(r1["forces"], r0["forces"])
+    assert any(name == "nccl_allreduce" for name, _ in ev.kernel_times())
