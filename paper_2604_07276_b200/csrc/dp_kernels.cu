@@ -117,6 +117,7 @@ struct Smem {
   float* dBd;
   int* z;
   double* red;
+  unsigned char* part;  // column-pass partials: [2][n_max] float4 + [2][n_max] float
 };
 
 __host__ __device__ inline size_t smem_layout(const DpArgs& a, int mode, unsigned char* base, Smem* out) {
@@ -141,6 +142,9 @@ __host__ __device__ inline size_t smem_layout(const DpArgs& a, int mode, unsigne
   s.dBd = reinterpret_cast<float*>(take(sizeof(float) * 4 * a.mr));
   s.z = reinterpret_cast<int*>(take(sizeof(int) * a.n_max));
   s.red = reinterpret_cast<double*>(take(sizeof(double) * 32));
+  // tcgen05 modes park the column-pass partials in the (idle) 96 KB operand stage; the
+  // SIMT head (one 64x64 tile) is too small, so it gets its own region
+  s.part = mode == 0 ? take(static_cast<size_t>(a.n_max) * 2 * (sizeof(float4) + sizeof(float))) : s.head;
   if (out) *out = s;
   return o;
 }
@@ -571,7 +575,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       {
         const int nh = (n + 1) >> 1;
         const int half_threads = blockDim.x >> 1;
-        float4* part = reinterpret_cast<float4*>(sm.head);          // [2][n] (g0..g3)
+        float4* part = reinterpret_cast<float4*>(sm.part);          // [2][n] (g0..g3)
         float* partw = reinterpret_cast<float*>(part + 2 * a.n_max);   // [2][n]
         const int h = threadIdx.x / half_threads;
         for (int j = threadIdx.x - h * half_threads; j < n; j += half_threads) {

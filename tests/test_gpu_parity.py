@@ -213,3 +213,51 @@ def test_nccl_collective_path_single_gpu(monkeypatch):
     assert r1["energy"] == r0["energy"]
     assert np.array_equal(r1["forces"], r0["forces"])
     assert any(name == "nccl_allreduce" for name, _ in ev.kernel_times())
+
+
+@pytest.mark.parametrize("prec", [nb.PREC_FP32, nb.PREC_FP32_SIMT])
+def test_large_neighbour_counts_multi_tile(prec):
+    """n > 128 rows per centre (rc = 8 territory): multi-tile per-centre GEMMs, the
+    unfused softmax path and n_max = 320, against the CPU oracle."""
+    import oracle as O
+    port = O.Port()
+    box, pos, sp = nb.synth_system(700, 0.42, 0.7, 21)
+    rc = 5.2
+    spec = nb.test_spec(rc, n_species=6)
+    spec.n_max = 320
+    m = nb.init_model(spec, 8)
+    ospec = O.test_spec(rc, n_species=6)
+    ospec["n_max"] = 320
+    h = port.model_init(ospec, 8)
+    ev = nb.DeviceEvaluator(m, n_ranks=1, precision=prec)
+    ev.set_debug(True)
+    r = ev.compute(pos, sp, box)
+    _, _, _, cnt = ev.debug_nlist(0, 320)
+    assert cnt.max() > 160, cnt.max()
+    o = port.evaluate(h, pos, sp, box)
+    tol = nb.TOLERANCE[prec]
+    assert abs(r["energy"] - o["energy"]) / abs(o["energy"]) <= tol
+    assert rel_err(r["forces"], o["forces"]) <= tol
+    assert rel_err(r["virial"], o["virial"]) <= tol
+    port.model_free(h)
+
+
+@pytest.mark.parametrize("rc", [4.0, 8.0])
+def test_paper_model_cutoff_sweep_spotcheck(rc):
+    """Paper-sized DPA-1 at rc = 4 (n_max 64) and rc = 8 (n_max 320): per-centre energies
+    of sampled centres against the CPU oracle, and rank invariance (1 vs 8 DD ranks)."""
+    import oracle as O
+    box, pos, sp = nb.synth_system(2000 if rc == 4.0 else 4200, 0.1, 0.9, 5)
+    m = nb.init_model(nb.paper_spec(rc), 1)
+    r1 = nb.DeviceEvaluator(m, n_ranks=1).compute(pos, sp, box)
+    r8 = nb.DeviceEvaluator(m, n_ranks=8 if rc == 4.0 else 1).compute(pos, sp, box)
+    assert np.array_equal(r1["atom_energy"], r8["atom_energy"])
+    port = O.Port()
+    h = port.model_init(dict(O.PAPER_SPEC, rc=rc, rcs=0.55 * rc, n_max=O.nmax_for_rc(rc)), 1)
+    counts, mem, img, d = port.neighbor_rows(h, pos, sp, box)
+    off = np.concatenate([[0], np.cumsum(counts)])
+    for c in (0, 777, len(pos) - 1):
+        rows = slice(off[c], off[c + 1])
+        e, _ = port.evaluate_center(h, int(sp[c]), d[rows], sp[mem[rows]])
+        assert abs(r1["atom_energy"][c] - e) <= 1e-5 * max(abs(e), 1e-2), (c, r1["atom_energy"][c], e)
+    port.model_free(h)
