@@ -284,6 +284,25 @@ def run_ours(args, ws, rank, local):
         pass
     achieved = f_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0
 
+    # ---- HBM-bound kernels: SURVEY 8(d) algorithmic bytes per launch / event time
+    hbm_peak = peaks.get("hbm_gbs", 6552.3)
+    sum_n = float(cnt.sum())
+    n_c = float(len(cnt))
+    members = float(stats["locals"] + stats["ghosts"])
+    n_max = nb.paper_spec(args.rc).n_max
+    alg = {
+        "neighbors": members * 36 + n_c * n_max * 4,                 # pos f64x3 + species + gid; nlist
+        "env": sum_n * (4 + 8 + 24 + 4 + 16 + 4) + n_c * 40,        # nlist, member, pos, species -> R f32x4, Z
+        "force_gather": sum_n * (24 + 4) + members * 24,            # f64 row grads + index; f64 member forces
+    }
+    hbm = {}
+    for k, b in alg.items():
+        ms = kernel_acc.get(k, 0.0) / args.steps
+        if ms > 0:
+            gbs = b / (ms * 1e-3) / 1e9
+            hbm[k] = {"algorithmic_bytes": b, "ms_per_launch": ms, "achieved_gbs": gbs, "peak_gbs": hbm_peak,
+                      "frac": gbs / hbm_peak}
+
     # ---- e2e through the host C-ABI entry point (pinned host buffers)
     h_pos = torch.from_numpy(pos).pin_memory().numpy()
     h_sp = torch.from_numpy(sp).pin_memory().numpy()
@@ -327,6 +346,7 @@ def run_ours(args, ws, rank, local):
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                          "forward": {"ms_per_launch": k_fwd, "algorithmic_flop": f_fwd,
                                      "achieved_tflops": f_fwd / (k_fwd * 1e-3) / 1e12 if k_fwd > 0 else 0.0}},
+            "hbm_kernels": hbm,
             "kernel_ms_per_step": {k: v / args.steps for k, v in sorted(kernel_acc.items(), key=lambda x: -x[1])},
             "rank0_stats": stats,
             "gpu_launches": int(launches),

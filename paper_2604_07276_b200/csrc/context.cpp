@@ -451,6 +451,10 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     dp.PTst = PTst_.p;
     dp.EMBst = EMBst_.p;
   }
+  Z_.ensure(static_cast<size_t>(ncen) * nmax + 1);
+  sig_.ensure(ncen + 1);
+  dp.Z = Z_.p;
+  dp.sig = sig_.p;
   dp.X = X_.p;
   dp.R = R_.p;
   dp.Ad = Ad_.p;
@@ -471,6 +475,9 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     CU(cudaMemsetAsync(fbuf.p, 0, 24 * sizeof(unsigned long long), st_));
     dp.prof = fbuf.p;
   }
+  tic("env");
+  launch_env(dp, st_);
+  toc();
   tic("centre_forward");
   launch_centre_forward(dp, grid, st_);
   toc();

@@ -85,7 +85,8 @@ class Context {
   DevBuf<int> nlist_, nn_, rlist_, rn_;
   DevBuf<float> X_, Ad_, Bd_, D_, dD_, scratch_, fitY_, fitd_, Ust_, PUst_, PTst_, EMBst_;
   DevBuf<float4> R_;
-  DevBuf<double> g_, vir_, e_, fmem_;
+  DevBuf<double> g_, vir_, e_, fmem_, sig_;
+  DevBuf<int> Z_;
   int* h_counts_ = nullptr;  // pinned
   std::vector<RankStat> stats_;
   std::vector<RankDebug> debug_;

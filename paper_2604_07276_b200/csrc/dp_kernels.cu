@@ -178,34 +178,19 @@ __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
   return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
 }
 
-// Row geometry of centre c: r, s (FP64), env row R = (s, s/r d) -> float.  Returns sigma.
+// Stage centre c's env rows (written by k_env) into shared memory; returns sigma.
 __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int& zi) {
-  const int cm = a.cen_member[c];
-  const int ca = a.m_atom[cm];
-  const int cs = a.m_shift[cm];
-  zi = a.species[ca];
-  const int* list = a.nlist + static_cast<size_t>(c) * a.n_max;
-  double sig = 0.0;
+  zi = a.species[a.m_atom[a.cen_member[c]]];
+  const float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
+  const int* Zg = a.Z + static_cast<size_t>(c) * a.n_max;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const int mj = list[k];
-    const int aj = a.m_atom[mj];
-    const int sj = a.m_shift[mj];
-    const int rel[3] = {shift_x(sj) - shift_x(cs), shift_y(sj) - shift_y(cs), shift_z(sj) - shift_z(cs)};
-    double d[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) d[q] = image_delta(a.pos[3 * aj + q], a.pos[3 * ca + q], rel[q], a.L[q]);
-    const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
-    double s, ds;
-    switch_fn(r, a.rcs, a.rc, s, ds);
-    const double sr = s / r;
-    const float4 R = make_float4(static_cast<float>(s), static_cast<float>(sr * d[0]),
-                                 static_cast<float>(sr * d[1]), static_cast<float>(sr * d[2]));
+    const float4 R = Rg[k];
     sm.R[k] = R;
-    sm.s[k] = static_cast<float>(s);
-    sm.z[k] = a.species[aj];
-    sig += s * s;
+    sm.s[k] = R.x;
+    sm.z[k] = Zg[k];
   }
-  return block_sum(sig, sm.red);
+  __syncthreads();
+  return a.sig[c];
 }
 
 // Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
@@ -331,8 +316,6 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
     const double sig = centre_rows(a, c, n, sm, zi);
     pc.mark(0);
     const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
-    float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) Rg[k] = sm.R[k];
     float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
     embed_forward(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, X);
     pc.mark(1);
@@ -724,6 +707,53 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   }
   pc.flush();
   mm.finish();
+}
+
+// ------------------------------------------------------------------------------------
+// Environment matrix (prepare_rows + switch_eval, dp_core.hpp:116-137, 200-223): warp
+// per centre, lanes over its rows.  d = image_delta(...) and r, s, ds/dr in exact FP64,
+// env row R = (s, s/r d) stored as float4 (coalesced 16-byte stores), neighbour species,
+// and sigma = sum_k s_k^2 (FP64, fixed-order warp reduction).
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_env(const __grid_constant__ DpArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= a.n_centres) return;
+  const int n = a.nn[c];
+  const int cm = a.cen_member[c];
+  const int ca = a.m_atom[cm];
+  const int cs = a.m_shift[cm];
+  const double pc[3] = {a.pos[3 * ca], a.pos[3 * ca + 1], a.pos[3 * ca + 2]};
+  const int* list = a.nlist + static_cast<size_t>(c) * a.n_max;
+  float4* R = a.R + static_cast<size_t>(c) * a.n_max;
+  int* Z = a.Z + static_cast<size_t>(c) * a.n_max;
+  double sig = 0.0;
+  for (int k = lane; k < n; k += 32) {
+    const int mj = list[k];
+    const int aj = a.m_atom[mj];
+    const int sj = a.m_shift[mj];
+    const int rel[3] = {shift_x(sj) - shift_x(cs), shift_y(sj) - shift_y(cs), shift_z(sj) - shift_z(cs)};
+    double d[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) d[q] = image_delta(a.pos[3 * aj + q], pc[q], rel[q], a.L[q]);
+    const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
+    double sw, ds;
+    switch_fn(r, a.rcs, a.rc, sw, ds);
+    const double sr = sw / r;
+    R[k] = make_float4(static_cast<float>(sw), static_cast<float>(sr * d[0]), static_cast<float>(sr * d[1]),
+                       static_cast<float>(sr * d[2]));
+    Z[k] = a.species[aj];
+    sig += sw * sw;
+  }
+  sig = warp_sum(sig);
+  if (lane == 0) a.sig[c] = sig;
+}
+
+void launch_env(const DpArgs& a, cudaStream_t st) {
+  if (a.n_centres == 0) return;
+  const long threads = static_cast<long>(a.n_centres) * 32;
+  k_env<<<static_cast<int>((threads + 255) / 256), 256, 0, st>>>(a);
+  count_launch();
 }
 
 template <int MODE>

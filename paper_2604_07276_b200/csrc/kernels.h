@@ -150,7 +150,9 @@ struct DpArgs {
   float* PTst;
   float* EMBst;
   size_t u_layer_stride, p_layer_stride, emb_centre_stride;
-  float4* R;            // [n_centres][n_max]
+  float4* R;            // [n_centres][n_max] env rows (s, s dx/r, s dy/r, s dz/r), k_env
+  int* Z;               // [n_centres][n_max] neighbour species, k_env
+  double* sig;          // [n_centres] sum_k s_k^2 (FP64), k_env
   float* Ad;            // [n_centres][M*4]
   float* Bd;            // [n_centres][4*mr]
   float* D;             // [n_centres][M*mr]
@@ -164,6 +166,9 @@ struct DpArgs {
 };
 size_t dp_scratch_floats(const DpArgs& a);
 size_t dp_smem_bytes(const DpArgs& a, int mode);
+// Environment matrix: FP64 geometry (image_delta, r, switch) -> float4 env rows, species,
+// and sigma = sum s^2 per centre; warp per centre, coalesced row stores.
+void launch_env(const DpArgs& a, cudaStream_t st);
 void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st);
 void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st);
 
