@@ -251,15 +251,18 @@ __device__ __forceinline__ void load_chunk(const float* __restrict__ X, int ld, 
       }
     }
   } else {
+    // 4x4 blocks (4 rows x 4 k); a warp takes a tile of 8 row-quads x 4 k-quads so that
+    // its loads are 128-byte rows and its swizzled 16-byte stores hit all 8 bank groups
     const int rq_n = R >> 2;
-    const int nb = rq_n * 8;
+    const int tiles_r = (rq_n + 7) >> 3;
+    const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int i = 0; i < MAXV / 4; ++i) {
-      const int b = tid + i * kThreads;
+      const int t = warp + i * (kThreads / 32);
 #pragma unroll
       for (int j = 0; j < 4; ++j) f.v[4 * i + j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (b < nb) {
-        const int rq = b % rq_n, kq = b / rq_n;
+      const int rq = 8 * (t % tiles_r) + (lane & 7), kq = 4 * (t / tiles_r) + (lane >> 3);
+      if (t < 2 * tiles_r && rq < rq_n) {
         const int gr = r0 + 4 * rq;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -283,12 +286,13 @@ __device__ __forceinline__ void store_chunk(int R, const Frag<MAXV>& f, uint8_t*
     }
   } else {
     const int rq_n = R >> 2;
-    const int nb = rq_n * 8;
+    const int tiles_r = (rq_n + 7) >> 3;
+    const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int i = 0; i < MAXV / 4; ++i) {
-      const int b = tid + i * kThreads;
-      if (b < nb) {
-        const int rq = b % rq_n, kq = b / rq_n;
+      const int t = warp + i * (kThreads / 32);
+      const int rq = 8 * (t % tiles_r) + (lane & 7), kq = 4 * (t / tiles_r) + (lane >> 3);
+      if (t < 2 * tiles_r && rq < rq_n) {
         const float4* w = &f.v[4 * i];
         st_split(hi, lo, sw128_off(4 * rq + 0, 4 * kq), make_float4(w[0].x, w[1].x, w[2].x, w[3].x), two);
         st_split(hi, lo, sw128_off(4 * rq + 1, 4 * kq), make_float4(w[0].y, w[1].y, w[2].y, w[3].y), two);
@@ -299,10 +303,6 @@ __device__ __forceinline__ void store_chunk(int R, const Frag<MAXV>& f, uint8_t*
   }
 }
 
-// PROMOTE > 0: every PROMOTE K-chunks the TMEM partial is added (FP32, round-to-nearest)
-// into a second TMEM region and the MMA accumulation restarts.  The tensor core's FP32
-// accumulation truncates (a relative bias growing ~1e-8 per accumulated product); short
-// chains keep long-K products (the K = 4096 fitting layer) at FP32 accuracy.
 // gemm2: C = epi(A1 B1 + A2 B2) accumulated in one TMEM tile (K1 and K2 may differ,
 // K2 = 0 for a single product); one epilogue for both products.
 // EK = epilogue kind: 0 scalar functor epi(m, n, float); 1 vector functor (also called
