@@ -74,6 +74,18 @@ __device__ __forceinline__ double block_sum(double v, double* scratch) {
   return t;
 }
 
+// Asynchronous L2 prefetch of a global range (one thread issues it; bulk-copy engine, no
+// registers held).  Used to pull a centre's forward stash out of HBM ahead of its use.
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~static_cast<uintptr_t>(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~static_cast<uintptr_t>(15);
+  while (a < e) {
+    const uint32_t sz = static_cast<uint32_t>((e - a) < 65536 ? (e - a) : 65536);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
+    a += sz;
+  }
+}
+
 // ---- scalar / float4 generic helpers for GEMM epilogue functors (called with a float
 // for single elements and a float4 for 4 consecutive, 16-byte aligned columns)
 __device__ __forceinline__ float vld(const float* p, float) { return *p; }

@@ -463,6 +463,8 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.dD = dD_.p;
   dp.g = g_.p;
   dp.vir = vir_.p;
+  static const int flags = getenv("NNMD_FLAGS") ? atoi(getenv("NNMD_FLAGS")) : 0;
+  dp.flags = flags;
   dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
   const int grid = std::max(1, std::min(ncen, 2 * n_sm_));  // two CTAs per SM (SIMT and tcgen05)
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);

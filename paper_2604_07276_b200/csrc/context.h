@@ -66,6 +66,7 @@ class Context {
   nnmd_b200_opts opts_;
   cudaStream_t st_ = nullptr;
   int n_sm_ = 148;
+
   DevBuf<float> weights_;
   NcclComm comm_ = nullptr;
   bool use_nccl_ = false;

@@ -45,8 +45,11 @@ __host__ __device__ inline size_t emb_floats(const DpArgs& a) {
 
 __host__ __device__ inline size_t align4(size_t x) { return (x + 3) & ~size_t(3); }
 
-__device__ inline Slot slot_of(const DpArgs& a, float* base) {
-  const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a), nm4 = align4(nm);
+// Offsets follow the centre's own n (not n_max), so the part of a slot a centre touches
+// is one compact prefix: the L2-persisting window over the slots (context.cpp) then
+// holds the live scratch and nothing else.
+__device__ inline Slot slot_of(const DpArgs& a, float* base, int n) {
+  const size_t nm = n, M2 = 2 * a.M, W = max_width(a), nm4 = align4(nm);
   Slot s;
   size_t o = 0;
   s.T = base + o;   o += nm * nm4;
@@ -76,13 +79,6 @@ struct Mm {
                                       Epi epi) {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
     else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
-  }
-  // Small GEMMs (the embedding net, N <= 128, K <= 128): the SIMT block GEMM on the idle
-  // tensor-core stage buffer beats tensor-core staging/epilogue latency at these sizes.
-  template <bool TA, bool TB, class Epi>
-  __device__ __forceinline__ void run_small(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
-                                            unsigned char* head, Epi epi) {
-    bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *reinterpret_cast<GemmSmem*>(head), epi);
   }
   // C = epi(A1 B1 + A2 B2) with one accumulator (tcgen05) or, on the SIMT path, two
   // passes through `acc` (ld N, must not alias the epilogue's sources).
@@ -279,6 +275,67 @@ __device__ void softmax_gate(int n, int ln, const float* S, int lds, float* PU, 
   }
 }
 
+// Backward row pass (warp per query row k, float4 over key columns j):
+//   dP = dP~ Theta, dC = dP~ P / sigma  ->  DP, DC (ld ln)
+//   t_k = sum_j dP P,  dsigma partial -sum_j dC C / sigma,  dR_k += sum_j dC_kj R_j
+// TS: dP~ (ld ldt; the T-GEMM's shared-memory accumulator tile, or DP itself).
+__device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const float* __restrict__ PU, float* DP,
+                             float* __restrict__ DC, float inv_sig, const Smem& sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = wid; k < n; k += nw) {
+    const float4 Rk = sm.R[k];
+    float t = 0.f, dsg = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+    for (int j4 = 4 * lane; j4 < n; j4 += 128) {
+      const float4 tv = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(k) * ldt + j4);
+      const float4 pu = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(k) * ln + j4);
+      const float tq[4] = {tv.x, tv.y, tv.z, tv.w};
+      const float pq[4] = {pu.x, pu.y, pu.z, pu.w};
+      float dpo[4], dco[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j4 + q;
+        dpo[q] = 0.f;
+        dco[q] = 0.f;
+        if (j < n) {
+          const float sj = sm.s[j];
+          const float4 Rj = sm.R[j];
+          const float C = dot4(Rk, Rj);
+          const float pv = sj * sj * pq[q];
+          const float dP = tq[q] * C * inv_sig;
+          const float dC = tq[q] * pv * inv_sig;
+          dpo[q] = dP;
+          dco[q] = dC;
+          dsg -= dC * C * inv_sig;
+          t += dP * pv;
+          g0 += dC * Rj.x;
+          g1 += dC * Rj.y;
+          g2 += dC * Rj.z;
+          g3 += dC * Rj.w;
+        }
+      }
+      const size_t kj = static_cast<size_t>(k) * ln + j4;
+      *reinterpret_cast<float4*>(DP + kj) = make_float4(dpo[0], dpo[1], dpo[2], dpo[3]);
+      *reinterpret_cast<float4*>(DC + kj) = make_float4(dco[0], dco[1], dco[2], dco[3]);
+    }
+    t = warp_sum(t);
+    dsg = warp_sum(dsg);
+    g0 = warp_sum(g0);
+    g1 = warp_sum(g1);
+    g2 = warp_sum(g2);
+    g3 = warp_sum(g3);
+    if (lane == 0) {
+      sm.t[k] = t;
+      sm.rowpart[k] = dsg;
+      float4 r = sm.dR[k];
+      r.x += g0;
+      r.y += g1;
+      r.z += g2;
+      r.w += g3;
+      sm.dR[k] = r;
+    }
+  }
+}
+
 }  // namespace
 
 size_t dp_scratch_floats(const DpArgs& a) {
@@ -307,7 +364,6 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
       mm.st.t_last = clock64();
     }
   }
-  const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
     const int n = a.nn[c];
@@ -411,12 +467,12 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       mm.st.t_last = clock64();
     }
   }
-  const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot);
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
     const int n = a.nn[c];
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
+    const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot, n);
     int zi;
     const double sig = centre_rows(a, c, n, sm, zi);
     pc.mark(0);
@@ -426,6 +482,13 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
     const float* dD = a.dD + static_cast<size_t>(c) * M * mr;
     const float* Ad = a.Ad + static_cast<size_t>(c) * M * 4;
     const float* Bd = a.Bd + static_cast<size_t>(c) * 4 * mr;
+    if (threadIdx.x == 0 && !(a.flags & 1)) {
+      // forward stash read first: final features (dR below) and the top layer's U
+      prefetch_l2(Xf, sizeof(float) * n * M);
+      if (a.n_attn > 0)
+        prefetch_l2(a.Ust + (a.n_attn - 1) * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2,
+                    sizeof(float) * n * M2);
+    }
     // dA[m][cc] = sum_q dD[m,q] B[cc,q];  dB[cc][q] = sum_m dD[m,q] A[m,cc]
     // (operands staged into shared memory with coalesced loads; the tensor-core stage
     // buffers are idle between GEMMs)
@@ -475,6 +538,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
     // dR_k = (X_k dA + X_k[:mr] dB^T) / sqrt(n_max): warp per row, lanes over features
     for (int k = wid; k < n; k += nw) {
       float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+#pragma unroll 4
       for (int m = lane; m < M; m += 32) {
         const float x = Xf[k * M + m];
         v0 += x * sm.dAd[m * 4 + 0];
@@ -503,58 +567,42 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       const float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
       const float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
       const float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
+      if (threadIdx.x == 0 && !(a.flags & 1)) {
+        // this layer's stash and the next (lower) layer's U are read from HBM below:
+        // start pulling them into L2 now
+        prefetch_l2(PUl, sizeof(float) * n * ln);
+        prefetch_l2(PTl, sizeof(float) * n * ln);
+        prefetch_l2(Xl, sizeof(float) * n * M);
+        if (l > 0) prefetch_l2(Ul - a.u_layer_stride, sizeof(float) * n * M2);
+        else prefetch_l2(a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, sizeof(float) * a.emb_centre_stride);
+      }
       pc.mark(2);
-      // T = dP~ = dY U_B^T
-      mm.template run<false, true>(n, n, M, dY, M, Ul + M, M2,
-                         [&](int k, int j, auto v) { vst(&sl.T[k * ln + j], v); });
-      __syncthreads();
-      pc.mark(5);
-      // row pass (warp per query row k, coalesced): dP = dP~ Theta, dC = dP~ P / sigma,
-      // t_k = sum_j dP P, dsigma partials, and the row half of the gate term
-      // dR_k += sum_j dC_kj R_j
-      for (int k = wid; k < n; k += nw) {
-        const float4 Rk = sm.R[k];
-        float t = 0.f, dsg = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
-        for (int j = lane; j < n; j += 32) {
-          const size_t kj = static_cast<size_t>(k) * ln + j;
-          const float sj = sm.s[j];
-          const float4 Rj = sm.R[j];
-          const float C = dot4(Rk, Rj);
-          const float dpt = sl.T[kj];
-          const float pv = sj * sj * PUl[kj];
-          const float dP = dpt * C * inv_sig;
-          const float dC = dpt * pv * inv_sig;
-          sl.T[kj] = dP;
-          sl.Qb[kj] = dC;
-          dsg -= dC * C * inv_sig;
-          t += dP * pv;
-          g0 += dC * Rj.x;
-          g1 += dC * Rj.y;
-          g2 += dC * Rj.z;
-          g3 += dC * Rj.w;
+      // T = dP~ = dY U_B^T, then the row pass (warp per query row k): dP = dP~ Theta,
+      // dC = dP~ P / sigma, t_k = sum_j dP P, dsigma partials, and the row half of the
+      // gate term dR_k += sum_j dC_kj R_j.  With tcgen05 and n <= 128 the row pass runs
+      // in the GEMM epilogue on the shared-memory accumulator tile.
+      bool fused_row = false;
+      if constexpr (MODE != 0) {
+        if (n <= 128 && !(a.flags & 2)) {
+          mm.template run<false, true, 0, 2>(n, n, M, dY, M, Ul + M, M2,
+                                             [&](const float* stg, int ldst, int, int, int, int) {
+                                               bwd_row_pass(n, ln, stg, ldst, PUl, sl.T, sl.Qb, inv_sig, sm);
+                                             });
+          fused_row = true;
         }
-        t = warp_sum(t);
-        dsg = warp_sum(dsg);
-        g0 = warp_sum(g0);
-        g1 = warp_sum(g1);
-        g2 = warp_sum(g2);
-        g3 = warp_sum(g3);
-        if (lane == 0) {
-          sm.t[k] = t;
-          sm.rowpart[k] = dsg;
-          float4 r = sm.dR[k];
-          r.x += g0;
-          r.y += g1;
-          r.z += g2;
-          r.w += g3;
-          sm.dR[k] = r;
-        }
+      }
+      if (!fused_row) {
+        mm.template run<false, true>(n, n, M, dY, M, Ul + M, M2,
+                                     [&](int k, int j, auto v) { vst(&sl.T[k * ln + j], v); });
+        __syncthreads();
+        pc.mark(5);
+        bwd_row_pass(n, ln, sl.T, ln, PUl, sl.T, sl.Qb, inv_sig, sm);
       }
       __syncthreads();
       pc.mark(6);
       // column pass (thread per key column j and k-half, coalesced across threads): dw_j
-      // of the s_j^2 softmax weights and the column half of the gate term
-      // dR_j += sum_k dC_kj R_k.  Two k-halves per column double the active threads.
+      // of the s_j^2 softmax weights, the column half of the gate term
+      // dR_j += sum_k dC_kj R_k, and dS = P o (dP - t) written in place over dP.
       {
         const int nh = (n + 1) >> 1;
         const int half_threads = blockDim.x >> 1;
@@ -563,11 +611,15 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         const int h = threadIdx.x / half_threads;
         for (int j = threadIdx.x - h * half_threads; j < n; j += half_threads) {
           float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+          const float sj2 = sm.s[j] * sm.s[j];
           const int kb = h * nh, ke = min(n, kb + nh);
 #pragma unroll 4
           for (int k = kb; k < ke; ++k) {
             const size_t kj = static_cast<size_t>(k) * ln + j;
-            dw += PUl[kj] * (sl.T[kj] - sm.t[k]);
+            const float pu = PUl[kj];
+            const float dpt = sl.T[kj] - sm.t[k];
+            dw += pu * dpt;
+            sl.T[kj] = sj2 * pu * dpt;
             const float dC = sl.Qb[kj];
             const float4 Rk = sm.R[k];
             g0 += dC * Rk.x;
@@ -599,15 +651,6 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
       __syncthreads();
       pc.mark(7);
-      // dS = P o (dP - t)
-      for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-        const int k = idx / n, j = idx - k * n;
-        const size_t kj = static_cast<size_t>(k) * ln + j;
-        const float sj = sm.s[j];
-        sl.T[kj] = sj * sj * PUl[kj] * (sl.T[kj] - sm.t[k]);
-      }
-      __syncthreads();
-      pc.mark(8);
       // dU_A = dS X ; dU_B = P~^T dY
       mm.template run<false, false>(n, M, n, sl.T, ln, Xl, M,
                           [&](int k, int m, auto v) { vst(&sl.dU[k * M2 + m], v); });
@@ -619,8 +662,18 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       {
         float* xo = dXn;
         const float* yi = dY;
-        mm.template run2<true, false, false, true>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
-                                                   [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&yi[k * M + m], v) + v); });
+        if (l > 0) {
+          mm.template run2<true, false, false, true>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
+                                                     [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&yi[k * M + m], v) + v); });
+        } else {
+          // bottom layer: the embedding's output tanh derivative (dp_core.hpp:580-583) is
+          // applied in the same epilogue, dX0 (1 - X0^2)
+          const float* x0 = X;
+          mm.template run2<true, false, false, true>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
+                                                     [=](int k, int m, auto v) {
+                                                       vst(&xo[k * M + m], (vld(&yi[k * M + m], v) + v) * vdtanh(vld(&x0[k * M + m], v)));
+                                                     });
+        }
       }
       __syncthreads();
       pc.mark(11);
@@ -628,13 +681,16 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       dY = dXn;
       dXn = tmp;
     }
-    // embedding backward (dp_core.hpp:580-596): recompute hidden activations
-    const float* X0 = X;
-    for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
-      const float y = X0[idx];
-      dY[idx] *= 1.f - y * y;
+    // embedding backward (dp_core.hpp:580-596) from the stored hidden activations; with
+    // attention layers the output tanh derivative was applied in the last dX epilogue
+    if (a.n_attn == 0) {
+      const float* X0 = X;
+      for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
+        const float y = X0[idx];
+        dY[idx] *= 1.f - y * y;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     {
       // offsets of the stored activations
       size_t offs[kMaxLayers];
@@ -911,7 +967,7 @@ __global__ void __launch_bounds__(256, 1) k_selftest_gemm(int M, int N, int K, c
                                                           const float* B, int ldb, float* C) {
   extern __shared__ __align__(1024) unsigned char st_smem_raw[];
   unsigned char* head = st_smem_raw + ((1024 - (tc::smem_u32(st_smem_raw) & 1023)) & 1023);
-  Mm<MODE, 1> mm;
+  Mm<MODE> mm;
   mm.init(head, 256);
   mm.template run<TA, TB, 0, 0>(M, N, K, A, lda, B, ldb, [&](int m, int n, float v) { C[static_cast<size_t>(m) * N + n] = v; });
   mm.finish();

@@ -163,6 +163,7 @@ struct DpArgs {
   size_t scratch_slot;  // floats per CTA slot
   int mode;             // 0 SIMT FP32, 1 3xTF32 tcgen05, 2 1xTF32 tcgen05
   unsigned long long* prof;  // optional per-phase cycle counters (thread 0 of each CTA)
+  int flags;            // experiment switches (NNMD_FLAGS): bit0 no L2 prefetch, bit1 unfused row pass
 };
 size_t dp_scratch_floats(const DpArgs& a);
 size_t dp_smem_bytes(const DpArgs& a, int mode);
