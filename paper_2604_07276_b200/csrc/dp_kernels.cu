@@ -61,8 +61,9 @@ __device__ inline Slot slot_of(const DpArgs& a, float* base, int n) {
 }
 
 // GEMM policy: MODE 0 = SIMT FP32 (gemm_simt.cuh), 1 = 3xTF32 tcgen05, 2 = 1xTF32 tcgen05.
-// NST = tensor-core pipeline stages: 1 for the per-centre kernels (small smem -> two
-// CTAs per SM hide each other's latency), 2 for the fitting-net GEMM tiles.
+// NST = 1: the per-centre kernels (96 KB head -> two CTAs per SM hide each other's
+// latency) run the TS-mode GEMM (A in TMEM, two B stages); NST = 2: the fitting-net tiles
+// run the SS-mode GEMM with 128-row FP32 promotion.
 template <int MODE, int NST = 1>
 struct Mm {
   GemmSmem* gs;
@@ -78,7 +79,14 @@ struct Mm {
   __device__ __forceinline__ void run(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                                       Epi epi) {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
-    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
+    else if constexpr (NST == 1 && PROMOTE == 0) {
+      // N > 128 would need a second A staging per 128-column tile in TS mode: the wide
+      // U = X [A|B] product stays on the SS path, which covers N = 256 in one tile
+      if (N <= tc::kTsN) tc::gemm_ts<TA, TB, MODE == 1 ? 3 : 1, EK>(st, M, N, K, A, lda, B, ldb, epi);
+      else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, 0, 1, EK>(st, M, N, K, A, lda, B, ldb, epi);
+    } else {
+      tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
+    }
   }
   // C = epi(A1 B1 + A2 B2) with one accumulator (tcgen05) or, on the SIMT path, two
   // passes through `acc` (ld N, must not alias the epilogue's sources).
@@ -90,7 +98,10 @@ struct Mm {
       __syncthreads();
       bgemm<TA2, TB2>(M, N, K2, A2, lda2, B2, ldb2, *gs, [&](int m, int n, float v) { epi(m, n, acc[m * N + n] + v); });
     } else {
-      tc::gemm2<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 0, NST, 1>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
+      if constexpr (NST == 1)
+        tc::gemm2_ts<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 1>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
+      else
+        tc::gemm2<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 0, NST, 1>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
     }
   }
 };

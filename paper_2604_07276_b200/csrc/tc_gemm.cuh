@@ -55,6 +55,7 @@ struct State {
   uint32_t waited[2];   // commits waited per stage
   unsigned long long* prof;  // optional: thread 0 accumulates cycles per GEMM stage (ids 0..7)
   long long t_last;
+  int dbg;  // microbenchmark switches (0 in production)
   __device__ __forceinline__ void tick(int id) {
     if (prof && threadIdx.x == 0) {
       const long long t = clock64();
@@ -173,6 +174,7 @@ __device__ __forceinline__ void init(State& st, Smem<NST>* sm, int cols) {
   st.waited[0] = st.waited[1] = 0;
   st.prof = nullptr;
   st.t_last = 0;
+  st.dbg = 0;
   if (threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&sm->tmem_base)),
@@ -464,6 +466,209 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
       fence_after();
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// TS-mode block GEMM: the A operand lives in TMEM, B in shared memory.
+//
+// Per 32-wide K chunk every thread loads 16 values of ONE A row (warp w: rows
+// 32*(w%4)+lane, k = 16*(w/4)..+15 of the chunk), splits hi/lo and writes them straight
+// into its TMEM lanes with tcgen05.st (no shared-memory traffic for A, and the MMA reads
+// no A bytes from shared memory); B is split into the swizzled smem stage as in gemm2.
+// Two stages (TMEM A + smem B, 32 KB per B stage): chunk c+1 is staged while the tensor
+// core works on chunk c.  TMEM map (256 columns): [0,128) accumulator, [128+64s, +32) A hi
+// and [160+64s, +32) A lo of stage s.  N is processed in 128-column tiles.
+// ---------------------------------------------------------------------------------------
+constexpr int kTsN = 128;
+constexpr uint32_t kTsA = 128;
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16_nowait(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
+// 16 values A(r, k0..k0+15) of one row (zero outside [0,M) x [0,K)).
+template <bool T>
+__device__ __forceinline__ void load_arow(const float* __restrict__ A, int lda, int M, int K, int r, int k0,
+                                          float (&v)[16]) {
+  if (!T) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + 4 * q;
+      float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < M && k < K) f = ld4(A + static_cast<size_t>(r) * lda + k, K - k);
+      v[4 * q] = f.x;
+      v[4 * q + 1] = f.y;
+      v[4 * q + 2] = f.z;
+      v[4 * q + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int k = k0 + j;
+      v[j] = (r < M && k < K) ? A[static_cast<size_t>(k) * lda + r] : 0.f;
+    }
+  }
+}
+
+template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int EK = 1, class Epi>
+__device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
+                                         const float* __restrict__ B, int ldb, int K2, const float* __restrict__ A2,
+                                         int lda2, const float* __restrict__ B2, int ldb2, Epi epi) {
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  constexpr bool two = NPASS > 1;
+  uint8_t* base = st.a[0][0];
+  const uint32_t lanes = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+  const int arow = 32 * (warp & 3) + lane;
+  const int akof = 16 * (warp >> 2);
+  for (int m0 = 0; m0 < M; m0 += kMT) {
+    for (int n0 = 0; n0 < N; n0 += kTsN) {
+      const int nrem = N - n0 < kTsN ? N - n0 : kTsN;
+      const int NT = (nrem + 15) & ~15;
+      const int nch1 = (K + kKC - 1) / kKC;
+      const int nch = nch1 + (K2 + kKC - 1) / kKC;
+      const uint32_t idesc = idesc_tf32(NT);
+      float av[16];
+      Frag<4> fb;
+      auto load = [&](int c) {
+        if (c < nch1) {
+          load_arow<TA>(A, lda, M, K, m0 + arow, c * kKC + akof, av);
+          load_chunk<!TB, 4>(B, ldb, N, K, n0, c * kKC, NT, fb);
+        } else {
+          load_arow<TA2>(A2, lda2, M, K2, m0 + arow, (c - nch1) * kKC + akof, av);
+          load_chunk<!TB2, 4>(B2, ldb2, N, K2, n0, (c - nch1) * kKC, NT, fb);
+        }
+      };
+      st.tick(-1);
+      load(0);
+      st.tick(0);
+      for (int c = 0; c < nch; ++c) {
+        const int s = c & 1;
+        wait_stage(st, s);  // MMAs of chunk c-2 (same TMEM A / smem B stage) have completed
+        st.tick(1);
+        {
+          float hi[16], lo[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            hi[j] = tf32_rn(av[j]);
+            lo[j] = av[j] - hi[j];
+          }
+          const uint32_t ta = st.tmem + lanes + kTsA + 64u * s + static_cast<uint32_t>(akof);
+          tmem_st16_nowait(ta, hi);
+          if (two) tmem_st16_nowait(ta + 32, lo);
+        }
+        uint8_t* bh = base + 32768 * s;
+        uint8_t* bl = bh + 16384;
+        if (c < nch1) store_chunk<!TB, 4>(NT, fb, bh, bl, two);
+        else store_chunk<!TB2, 4>(NT, fb, bh, bl, two);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        st.tick(2);
+        fence_before();
+        fence_proxy_async();
+        __syncthreads();
+        st.tick(3);
+        if (tid == 0) {
+          fence_after();
+          const uint32_t ah = st.tmem + kTsA + 64u * s, al = ah + 32;
+          const uint32_t b0 = smem_u32(bh), b1 = smem_u32(bl);
+#pragma unroll
+          for (int kk = 0; kk < kKC / 8; ++kk) {
+            const uint32_t acc0 = (c > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32_ts(st.tmem, ah + 8 * kk, kmajor_sw128_desc(b0 + 32 * kk), idesc, acc0);
+            if (NPASS > 1) {
+              mma_tf32_ts(st.tmem, ah + 8 * kk, kmajor_sw128_desc(b1 + 32 * kk), idesc, 1u);
+              mma_tf32_ts(st.tmem, al + 8 * kk, kmajor_sw128_desc(b0 + 32 * kk), idesc, 1u);
+            }
+          }
+          mma_commit(&st.bar[s]);
+        }
+        ++st.uses[s];
+        st.tick(4);
+        if (c + 1 < nch) load(c + 1);  // next chunk's global loads overlap this chunk's MMAs
+        st.tick(0);
+      }
+      wait_stage(st, 0);
+      wait_stage(st, 1);
+      fence_after();
+      st.tick(5);
+      // ---- epilogue (accumulator columns [0, NT)): TMEM -> registers -> shared (row-major,
+      // padded) -> coalesced epi over rows; the B stages are free now
+      float* stg = reinterpret_cast<float*>(base);
+      const int q = warp & 3;
+      const int mrows = M - m0 < kMT ? M - m0 : kMT;
+      const int CB = NT;
+      const int ldst = CB + 4;
+      const int half = ((CB >> 1) + 15) & ~15;
+      const int cbeg = (warp < 4) ? 0 : half;
+      const int cend = (warp < 4) ? half : CB;
+      float* srow = stg + static_cast<size_t>(q * 32 + lane) * ldst;
+      for (int c0 = cbeg; c0 < cend; c0 += 16) {
+        float v[16];
+        tmem_ld16(st.tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(c0), v);
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(srow + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+      fence_before();
+      __syncthreads();
+      st.tick(6);
+      const int ncols = nrem;
+      if constexpr (EK == 2) {
+        epi(stg, ldst, mrows, ncols, m0, n0);
+      } else if constexpr (EK == 1) {
+        const int nq = ncols >> 2;
+        for (int r = warp; r < mrows; r += 4 * (kThreads / 32))
+          for (int qd = lane; qd < nq; qd += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rr = r + u * (kThreads / 32);
+              if (rr < mrows)
+                epi(m0 + rr, n0 + 4 * qd, *reinterpret_cast<const float4*>(stg + static_cast<size_t>(rr) * ldst + 4 * qd));
+            }
+          }
+        for (int e = threadIdx.x; e < mrows * (ncols - 4 * nq); e += kThreads) {
+          const int rr = e / (ncols - 4 * nq), cc = 4 * nq + e % (ncols - 4 * nq);
+          epi(m0 + rr, n0 + cc, stg[static_cast<size_t>(rr) * ldst + cc]);
+        }
+      } else {
+        for (int r = warp; r < mrows; r += 4 * (kThreads / 32))
+          for (int n = lane; n < ncols; n += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rr = r + u * (kThreads / 32);
+              if (rr < mrows) epi(m0 + rr, n0 + n, stg[static_cast<size_t>(rr) * ldst + n]);
+            }
+          }
+      }
+      __syncthreads();
+      st.tick(7);
+      fence_after();
+    }
+  }
+}
+
+template <bool TA, bool TB, int NPASS, int EK = 1, class Epi>
+__device__ __forceinline__ void gemm_ts(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
+                                        const float* __restrict__ B, int ldb, Epi epi) {
+  gemm2_ts<TA, TB, TA, TB, NPASS, EK>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi);
 }
 
 template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, int EK = 1, class Epi>
