@@ -104,6 +104,32 @@ nnmd_status nnmd_b200_compute_device(nnmd_b200* ctx, int64_t n, const double* d_
                                      const double box[3], const uint8_t periodic[3],
                                      double* d_out);
 
+/* ---- device-resident MD loop (run_md, engine.cpp:143-211; MDConfig, engine.hpp:99-107) */
+typedef struct {
+  double dt;                 /* > 0 */
+  long n_steps;
+  long equil_steps;          /* velocity rescaling during the first equil_steps ... */
+  double target_temperature; /* ... to this temperature (<= 0 disables) ... */
+  long rescale_every;        /* ... every rescale_every steps */
+} nnmd_md_config;
+
+/* n_steps of NVE leap-frog (leapfrog_step, engine.cpp:91-100: v += (dt/m) F, r += dt v,
+ * wrapped) with this context's DPA-1 forces.  Positions and velocities stay on the device
+ * for the whole run (one H2D before, one D2H after); each process integrates its own
+ * replicated copy, so no position collective is needed.  coords/velocities are updated in
+ * place; potential[k] / total[k] (may be NULL) receive run_md's per-step potential energy
+ * and potential + on-step kinetic energy (mid-point velocities).  A non-finite force fails
+ * with NNMD_ERROR "run_md: non-finite force from provider 'nnmd_b200' at step k". */
+nnmd_status nnmd_b200_run_md(nnmd_b200* ctx, int64_t n, double* coords, double* velocities,
+                             const double* masses, const int32_t* types, const int64_t* gids,
+                             const double box[3], const uint8_t periodic[3], const nnmd_md_config* cfg,
+                             double* potential, double* total);
+/* Same on device buffers; d_energies[2k] = potential, d_energies[2k+1] = total of step k. */
+nnmd_status nnmd_b200_run_md_device(nnmd_b200* ctx, int64_t n, double* d_coords, double* d_velocities,
+                                    const double* d_masses, const int32_t* d_types, const int64_t* d_gids,
+                                    const double box[3], const uint8_t periodic[3],
+                                    const nnmd_md_config* cfg, double* d_energies);
+
 /* Per-rank statistics of the last compute (RankStats, decomp.hpp:133-142):
  * counts = {locals, ghosts, centres, route_entries}; ms = {dd, neighbor, inference, comm}
  * measured with CUDA events on the rank's stream. */

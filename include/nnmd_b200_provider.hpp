@@ -100,6 +100,47 @@ class GpuDpProvider : public ForceProvider {
 
   const double* last_virial() const { return virial_; }
 
+  // Device-resident variant of nnmd::run_md (engine.cpp:143-211) for this provider alone:
+  // positions and velocities stay on the GPU for all n_steps (one copy in, one copy out),
+  // the leap-frog step runs as a kernel.  Same RunSummary fields (potential_energy,
+  // total_energy, elapsed_seconds, throughput); trajectory output is not written.
+  RunSummary run_md(AtomSet& atoms, const SimBox& box, const MDConfig& config) {
+    require(config.dt > 0.0, "run_md: dt must be > 0");
+    require(config.n_steps >= 0, "run_md: n_steps must be >= 0");
+    require(group_.empty() && opts_.species_map.empty(),
+            "GpuDpProvider::run_md: group masks and species maps need nnmd::run_md");
+    atoms.validate();
+    const std::size_t n = atoms.size();
+    std::vector<double> x(3 * n), v(3 * n);
+    std::vector<std::int32_t> sp(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      for (int a = 0; a < 3; ++a) {
+        x[3 * i + a] = atoms.positions[i][a];
+        v[3 * i + a] = atoms.velocities[i][a];
+      }
+      sp[i] = atoms.species[i];
+    }
+    const double L[3] = {box.lengths.x, box.lengths.y, box.lengths.z};
+    const std::uint8_t per[3] = {box.periodic[0], box.periodic[1], box.periodic[2]};
+    nnmd_md_config c{config.dt, config.n_steps, config.equil_steps, config.target_temperature,
+                     config.rescale_every};
+    RunSummary s;
+    s.dt = config.dt;
+    s.potential_energy.resize(static_cast<std::size_t>(config.n_steps));
+    s.total_energy.resize(static_cast<std::size_t>(config.n_steps));
+    const double t0 = TraceSink::now();
+    check(nnmd_b200_run_md(ctx_, static_cast<std::int64_t>(n), x.data(), v.data(), atoms.masses.data(), sp.data(),
+                           atoms.global_ids.data(), L, per, &c, s.potential_energy.data(), s.total_energy.data()));
+    s.elapsed_seconds = TraceSink::now() - t0;
+    s.steps = config.n_steps;
+    if (s.steps > 0 && s.elapsed_seconds > 0) s.throughput = throughput_per_day(s.steps, s.dt, s.elapsed_seconds);
+    for (std::size_t i = 0; i < n; ++i) {
+      atoms.positions[i] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+      atoms.velocities[i] = {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+    }
+    return s;
+  }
+
  private:
   static void check(nnmd_status st) {
     if (st == NNMD_OK) return;

@@ -54,8 +54,23 @@ int main(int argc, char** argv) {
   go.n_ranks = decomposed ? 2 : 1;
   GpuDpProvider gpu(model, go);
 
+  AtomSet a_dev = cfg.atoms;
   const RunSummary s_ref = run_md(a_ref, cfg.box, md, {&ref});
   const RunSummary s_gpu = run_md(a_gpu, cfg.box, md, {&gpu});
+  // device-resident loop of the same provider: identical forces from identical positions
+  // and the reference's integrator arithmetic -> the trajectory must be bit-identical
+  const RunSummary s_dev = gpu.run_md(a_dev, cfg.box, md);
+  double dev_dx = 0, dev_dv = 0, dev_de = 0, dev_dt = 0;
+  for (std::size_t i = 0; i < a_gpu.size(); ++i)
+    for (int c = 0; c < 3; ++c) {
+      dev_dx = std::max(dev_dx, std::abs(a_gpu.positions[i][c] - a_dev.positions[i][c]));
+      dev_dv = std::max(dev_dv, std::abs(a_gpu.velocities[i][c] - a_dev.velocities[i][c]));
+    }
+  for (long k = 0; k < steps; ++k) {
+    dev_de = std::max(dev_de, std::abs(s_gpu.potential_energy[k] - s_dev.potential_energy[k]));
+    dev_dt = std::max(dev_dt, std::abs(s_gpu.total_energy[k] - s_dev.total_energy[k]) /
+                                  std::max(std::abs(s_gpu.total_energy[k]), 1e-300));
+  }
   double de = 0, escale = 0, dx = 0;
   for (long k = 0; k < steps; ++k) {
     de = std::max(de, std::abs(s_ref.potential_energy[k] - s_gpu.potential_energy[k]));
@@ -69,8 +84,13 @@ int main(int argc, char** argv) {
     }
   std::printf(
       "{\"provider\": \"%s\", \"steps\": %d, \"atoms\": %zu, \"max_rel_energy_diff\": %.3e, "
-      "\"max_position_diff\": %.3e, \"e_ref_step0\": %.10f, \"e_gpu_step0\": %.10f}\n",
+      "\"max_position_diff\": %.3e, \"e_ref_step0\": %.10f, \"e_gpu_step0\": %.10f, "
+      "\"device_loop_position_diff\": %.3e, \"device_loop_velocity_diff\": %.3e, "
+      "\"device_loop_potential_diff\": %.3e, \"device_loop_total_rel_diff\": %.3e}\n",
       gpu.name().c_str(), steps, a_ref.size(), de / std::max(escale, 1e-300), dx,
-      s_ref.potential_energy[0], s_gpu.potential_energy[0]);
-  return (de / std::max(escale, 1e-300) < 1e-5 && dx < 1e-6) ? 0 : 1;
+      s_ref.potential_energy[0], s_gpu.potential_energy[0], dev_dx, dev_dv, dev_de, dev_dt);
+  return (de / std::max(escale, 1e-300) < 1e-5 && dx < 1e-6 && dev_dx == 0.0 && dev_dv == 0.0 && dev_de == 0.0 &&
+          dev_dt < 1e-13)
+             ? 0
+             : 1;
 }

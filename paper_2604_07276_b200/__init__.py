@@ -84,6 +84,11 @@ _u8p = C.POINTER(C.c_uint8)
 _lib = None
 
 
+class _MdCfg(C.Structure):
+    _fields_ = [("dt", C.c_double), ("n_steps", C.c_long), ("equil_steps", C.c_long),
+                ("target_temperature", C.c_double), ("rescale_every", C.c_long)]
+
+
 def lib():
     """The loaded libnnmd_b200.so (ImportError if it has not been built)."""
     global _lib
@@ -108,6 +113,10 @@ def lib():
     L.nnmd_b200_nccl_unique_id.argtypes = [C.c_void_p]
     L.nnmd_b200_compute.argtypes = [C.c_void_p, C.c_int64, _dp, _ip, _i64p, _dp, _u8p, _dp, _dp, _dp, _dp]
     L.nnmd_b200_compute_device.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, _dp, _u8p, C.c_void_p]
+    L.nnmd_b200_run_md.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, _ip, _i64p, _dp, _u8p,
+                                   C.POINTER(_MdCfg), _dp, _dp]
+    L.nnmd_b200_run_md_device.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, _dp, _u8p, C.POINTER(_MdCfg), C.c_void_p]
     L.nnmd_b200_rank_stats.argtypes = [C.c_void_p, C.c_int, _i64p, _dp]
     L.nnmd_b200_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_char_p), _dp, C.c_int]
     L.nnmd_b200_set_debug.argtypes = [C.c_void_p, C.c_int]
@@ -293,6 +302,39 @@ class DeviceEvaluator:
                                        per.ctypes.data_as(_u8p), C.byref(e), _d(f), _d(w), _d(ae)))
         return dict(energy=e.value, forces=f, virial=w.reshape(3, 3), atom_energy=ae)
 
+    def run_md(self, coords, velocities, masses, types, box, dt, n_steps, gids=None, periodic=None,
+               equil_steps=0, target_temperature=-1.0, rescale_every=10):
+        """Device-resident MD loop (run_md, engine.cpp:143-211).  coords/velocities
+        (float64 [n,3], C-contiguous) are updated in place; returns (potential[n_steps],
+        total[n_steps])."""
+        for a in (coords, velocities):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+                raise Error("run_md: coords and velocities must be C-contiguous float64 arrays")
+        n = len(coords)
+        masses = np.ascontiguousarray(masses, dtype=np.float64)
+        types = np.ascontiguousarray(types, dtype=np.int32)
+        g = None if gids is None else np.ascontiguousarray(gids, dtype=np.int64)
+        box = np.ascontiguousarray(box, dtype=np.float64)
+        per = np.ascontiguousarray([1, 1, 1] if periodic is None else periodic, dtype=np.uint8)
+        cfg = _MdCfg(dt, n_steps, equil_steps, target_temperature, rescale_every)
+        pot = np.zeros(max(n_steps, 1))
+        tot = np.zeros(max(n_steps, 1))
+        _check(lib().nnmd_b200_run_md(self._h, n, _d(coords), _d(velocities), _d(masses), types.ctypes.data_as(_ip),
+                                      None if g is None else g.ctypes.data_as(_i64p), _d(box),
+                                      per.ctypes.data_as(_u8p), C.byref(cfg), _d(pot), _d(tot)))
+        return pot[:n_steps], tot[:n_steps]
+
+    def run_md_device(self, n: int, d_coords: int, d_vel: int, d_mass: int, d_types: int, d_gids: int, box,
+                      dt, n_steps, d_energies: int, periodic=None, equil_steps=0, target_temperature=-1.0,
+                      rescale_every=10):
+        """Device pointers; d_energies[2k] = potential, [2k+1] = total energy of step k."""
+        box = np.ascontiguousarray(box, dtype=np.float64)
+        per = np.ascontiguousarray([1, 1, 1] if periodic is None else periodic, dtype=np.uint8)
+        cfg = _MdCfg(dt, n_steps, equil_steps, target_temperature, rescale_every)
+        _check(lib().nnmd_b200_run_md_device(self._h, n, C.c_void_p(d_coords), C.c_void_p(d_vel),
+                                             C.c_void_p(d_mass), C.c_void_p(d_types), C.c_void_p(d_gids), _d(box),
+                                             per.ctypes.data_as(_u8p), C.byref(cfg), C.c_void_p(d_energies)))
+
     def compute_device(self, n: int, d_coords: int, d_types: int, d_gids: int, box, d_out: int, periodic=None):
         """Device pointers in/out; d_out = [E, W(9), F(3n), ae(n)] float64."""
         box = np.ascontiguousarray(box, dtype=np.float64)
@@ -458,6 +500,53 @@ class DpProvider(ForceProvider):
                              gids=np.asarray(atoms.global_ids)[idx], periodic=[int(p) for p in box.periodic])
         forces[idx] = r["forces"]
         return ProviderResult(r["energy"], forces, r["virial"])
+
+
+@dataclasses.dataclass
+class MDConfig:
+    """nnmd::MDConfig (engine.hpp:99-107)."""
+    dt: float = 0.002
+    n_steps: int = 0
+    output_every: int = 0  # trajectory cadence (file output is out of scope here)
+    equil_steps: int = 0
+    target_temperature: float = -1.0
+    rescale_every: int = 10
+
+
+@dataclasses.dataclass
+class RunSummary:
+    """nnmd::RunSummary (engine.hpp:109-117)."""
+    steps: int
+    dt: float
+    elapsed_seconds: float
+    throughput: float
+    potential_energy: np.ndarray
+    total_energy: np.ndarray
+
+
+def run_md(atoms: AtomSet, box: SimBox, config: MDConfig, provider: "DpProvider") -> RunSummary:
+    """nnmd::run_md (engine.cpp:143-211) with one DpProvider, on the device: positions and
+    velocities stay in HBM for the whole run.  atoms.positions / atoms.velocities are
+    updated in place."""
+    import time
+    if config.dt <= 0:
+        raise Error("run_md: dt must be > 0")
+    if config.n_steps < 0:
+        raise Error("run_md: n_steps must be >= 0")
+    if provider.group is not None or len(provider.opts.species_map):
+        raise Error("run_md (device loop): group masks and species maps need the host loop")
+    pos = np.ascontiguousarray(atoms.positions, dtype=np.float64)
+    vel = np.ascontiguousarray(atoms.velocities, dtype=np.float64)
+    t0 = time.perf_counter()
+    pot, tot = provider._ev.run_md(pos, vel, atoms.masses, atoms.species, box.lengths, config.dt, config.n_steps,
+                                   gids=atoms.global_ids, periodic=[int(p) for p in box.periodic],
+                                   equil_steps=config.equil_steps, target_temperature=config.target_temperature,
+                                   rescale_every=config.rescale_every)
+    el = time.perf_counter() - t0
+    atoms.positions[...] = pos
+    atoms.velocities[...] = vel
+    thr = config.n_steps * config.dt / el * 86400.0 if el > 0 else 0.0
+    return RunSummary(config.n_steps, config.dt, el, thr, pot, tot)
 
 
 def header_functions() -> list:

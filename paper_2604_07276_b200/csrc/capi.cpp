@@ -163,6 +163,36 @@ nnmd_status nnmd_b200_compute(nnmd_b200* h, int64_t n, const double* coords, con
   });
 }
 
+static nb::Context::MdConfig md_cfg(const nnmd_md_config* c) {
+  nb::require(c != nullptr, "nnmd_b200_run_md: null config");
+  return nb::Context::MdConfig{c->dt, c->n_steps, c->equil_steps, c->target_temperature, c->rescale_every};
+}
+
+nnmd_status nnmd_b200_run_md(nnmd_b200* h, int64_t n, double* coords, double* velocities, const double* masses,
+                             const int32_t* types, const int64_t* gids, const double box[3],
+                             const uint8_t periodic[3], const nnmd_md_config* cfg, double* potential,
+                             double* total) {
+  return guarded([&] {
+    nb::require(box && (n == 0 || (coords && velocities && masses && types)), "nnmd_b200_run_md: null argument");
+    const uint8_t per_default[3] = {1, 1, 1};
+    C(h).run_md_host(n, coords, velocities, masses, types, gids, box, periodic ? periodic : per_default,
+                     md_cfg(cfg), potential, total);
+  });
+}
+
+nnmd_status nnmd_b200_run_md_device(nnmd_b200* h, int64_t n, double* d_coords, double* d_velocities,
+                                    const double* d_masses, const int32_t* d_types, const int64_t* d_gids,
+                                    const double box[3], const uint8_t periodic[3], const nnmd_md_config* cfg,
+                                    double* d_energies) {
+  return guarded([&] {
+    nb::require(box && d_gids && d_energies && (n == 0 || (d_coords && d_velocities && d_masses && d_types)),
+                "nnmd_b200_run_md_device: null argument");
+    const uint8_t per_default[3] = {1, 1, 1};
+    C(h).run_md(n, d_coords, d_velocities, d_masses, d_types, d_gids, box, periodic ? periodic : per_default,
+                md_cfg(cfg), d_energies);
+  });
+}
+
 nnmd_status nnmd_b200_compute_device(nnmd_b200* h, int64_t n, const double* d_coords,
                                      const int32_t* d_types, const int64_t* d_gids,
                                      const double box[3], const uint8_t periodic[3], double* d_out) {

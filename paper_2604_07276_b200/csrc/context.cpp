@@ -677,4 +677,91 @@ void Context::compute_host(long n, const double* pos, const int* types, const in
   if (virial) std::memcpy(virial, head + 1, 9 * sizeof(double));
 }
 
+// ---- device-resident MD loop ---------------------------------------------------------
+void Context::run_md(long n, double* d_pos, double* d_vel, const double* d_mass, const int* d_types,
+                     const int64_t* d_gid, const double box[3], const uint8_t periodic[3], const MdConfig& cfg,
+                     double* d_rec) {
+  require(cfg.dt > 0.0, "run_md: dt must be > 0");
+  require(cfg.n_steps >= 0, "run_md: n_steps must be >= 0");
+  out_.ensure(10 + 4 * static_cast<size_t>(n));
+  md_ke_.ensure(static_cast<size_t>(n) + 1);
+  md_sum_.ensure(1);
+  md_err_.ensure(1);
+  CU(cudaMemsetAsync(md_err_.p, 0x7f, sizeof(int), st_));
+  MdArgs ma{};
+  ma.n = static_cast<int>(n);
+  ma.pos = d_pos;
+  ma.vel = d_vel;
+  ma.mass = d_mass;
+  ma.F = out_.p + 10;
+  ma.dt = cfg.dt;
+  for (int a = 0; a < 3; ++a) {
+    ma.L[a] = box[a];
+    ma.per[a] = periodic[a] ? 1 : 0;
+  }
+  ma.ke_atom = md_ke_.p;
+  ma.err = md_err_.p;
+  auto check_forces = [&] {
+    int bad = 0;
+    CU(cudaMemcpyAsync(&bad, md_err_.p, sizeof bad, cudaMemcpyDeviceToHost, st_));
+    CU(cudaStreamSynchronize(st_));
+    if (bad != 0x7f7f7f7f)
+      throw Error("run_md: non-finite force from provider 'nnmd_b200' at step " + std::to_string(bad));
+  };
+  for (long step = 0; step < cfg.n_steps; ++step) {
+    if (step > 0) check_forces();  // the previous step's forces were finite
+    // forces of the current positions (replicated on every process after the all-reduce,
+    // so each process integrates its own copy: no position collective is needed)
+    compute_device(n, d_pos, d_types, d_gid, box, periodic, out_.p);
+    ma.step = static_cast<int>(step);
+    launch_leapfrog(ma, st_);
+    launch_energy_record(md_ke_.p, ma.n, out_.p, d_rec, step, st_);
+    if (cfg.target_temperature > 0.0 && step < cfg.equil_steps && cfg.rescale_every > 0 &&
+        (step + 1) % cfg.rescale_every == 0)
+      launch_rescale(ma.n, d_vel, d_mass, md_ke_.p, md_sum_.p, cfg.target_temperature, st_);
+    check_launch("md_step");
+  }
+  check_forces();
+}
+
+void Context::run_md_host(long n, double* pos, double* vel, const double* mass, const int* types,
+                          const int64_t* gid, const double box[3], const uint8_t periodic[3], const MdConfig& cfg,
+                          double* potential, double* total) {
+  for (long i = 0; i < n; ++i) {
+    require(types[i] >= 0 && types[i] < model_.ns, "dd_evaluate: species id outside the model's species table");
+    require(mass[i] > 0.0, "AtomSet: masses must be positive");
+  }
+  pos_.ensure(3 * static_cast<size_t>(n) + 3);
+  types_.ensure(static_cast<size_t>(n) + 1);
+  gid_.ensure(static_cast<size_t>(n) + 1);
+  md_vel_.ensure(3 * static_cast<size_t>(n) + 3);
+  md_mass_.ensure(static_cast<size_t>(n) + 1);
+  md_rec_.ensure(2 * static_cast<size_t>(std::max(cfg.n_steps, 1L)));
+  std::vector<int64_t> iota;
+  if (!gid) {
+    iota.resize(static_cast<size_t>(n));
+    for (long i = 0; i < n; ++i) iota[static_cast<size_t>(i)] = i;
+    gid = iota.data();
+  }
+  if (n) {
+    CU(cudaMemcpyAsync(pos_.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st_));
+    CU(cudaMemcpyAsync(md_vel_.p, vel, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st_));
+    CU(cudaMemcpyAsync(md_mass_.p, mass, n * sizeof(double), cudaMemcpyHostToDevice, st_));
+    CU(cudaMemcpyAsync(types_.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st_));
+    CU(cudaMemcpyAsync(gid_.p, gid, n * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+  }
+  run_md(n, pos_.p, md_vel_.p, md_mass_.p, types_.p, gid_.p, box, periodic, cfg, md_rec_.p);
+  std::vector<double> rec(2 * static_cast<size_t>(cfg.n_steps));
+  if (cfg.n_steps) CU(cudaMemcpyAsync(rec.data(), md_rec_.p, rec.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (n) {
+    CU(cudaMemcpyAsync(pos, pos_.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CU(cudaMemcpyAsync(vel, md_vel_.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  }
+  CU(cudaStreamSynchronize(st_));
+  for (long k = 0; k < cfg.n_steps; ++k) {
+    if (potential) potential[k] = rec[2 * static_cast<size_t>(k)];
+    if (total) total[k] = rec[2 * static_cast<size_t>(k) + 1];
+  }
+}
+
 }  // namespace nb

@@ -48,6 +48,23 @@ class Context {
                     const double box[3], const uint8_t periodic[3], double* energy,
                     double* forces, double* virial, double* atom_energy);
 
+  // Device-resident MD loop (run_md, engine.cpp:143-211): n_steps of leap-frog on
+  // positions/velocities that stay on the device; rec[2k] = potential, rec[2k+1] = total
+  // energy of step k (device).  Throws Error on a non-finite force like run_md.
+  struct MdConfig {
+    double dt;
+    long n_steps;
+    long equil_steps;
+    double target_temperature;
+    long rescale_every;
+  };
+  void run_md(long n, double* d_pos, double* d_vel, const double* d_mass, const int* d_types,
+              const int64_t* d_gid, const double box[3], const uint8_t periodic[3], const MdConfig& cfg,
+              double* d_rec);
+  void run_md_host(long n, double* pos, double* vel, const double* mass, const int* types, const int64_t* gid,
+                   const double box[3], const uint8_t periodic[3], const MdConfig& cfg, double* potential,
+                   double* total);
+
   cudaStream_t stream() const { return st_; }
   const RankStat& stat(int r) const { return stats_.at(static_cast<size_t>(r)); }
   int n_ranks() const { return opts_.n_ranks; }
@@ -76,6 +93,9 @@ class Context {
   DevBuf<int> types_;
   DevBuf<int64_t> gid_;
   DevBuf<double> h_pinned_dummy_;
+  // MD loop state (host API path) and scratch
+  DevBuf<double> md_vel_, md_mass_, md_ke_, md_rec_, md_sum_;
+  DevBuf<int> md_err_;
   // step-global
   DevBuf<int> owner_, err_;
   // per rank (reused across virtual ranks)

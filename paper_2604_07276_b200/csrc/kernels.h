@@ -190,6 +190,28 @@ struct FitArgs {
 };
 void launch_fit(const FitArgs& a, cudaStream_t st);
 
+// ---------------------------------------------------------------- MD loop -------------
+struct MdArgs {
+  int n;
+  double* pos;          // [n][3], wrapped in place
+  double* vel;          // [n][3]
+  const double* mass;   // [n]
+  const double* F;      // [n][3] forces of this step
+  double dt;
+  double L[3];
+  int per[3];
+  double* ke_atom;      // [n] on-step kinetic energy per atom (mid-point velocity)
+  int* err;             // atomicMin(step) on a non-finite force
+  int step;
+};
+void launch_leapfrog(const MdArgs& a, cudaStream_t st);
+// rec[2 step] = epot[0], rec[2 step + 1] = epot[0] + sum(ke_atom)  (deterministic)
+void launch_energy_record(const double* ke_atom, int n, const double* epot, double* rec, long step,
+                          cudaStream_t st);
+// velocity rescaling to `temperature` from the stored velocities' kinetic energy
+void launch_rescale(int n, double* vel, const double* mass, double* ke_atom, double* ke_sum, double temperature,
+                    cudaStream_t st);
+
 // One-CTA test of the block GEMM building block (device pointers), mode as DpArgs::mode.
 void selftest_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A, int lda, const float* B,
                    int ldb, float* C);
