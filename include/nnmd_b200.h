@@ -130,6 +130,38 @@ nnmd_status nnmd_b200_run_md_device(nnmd_b200* ctx, int64_t n, double* d_coords,
                                     const double box[3], const uint8_t periodic[3],
                                     const nnmd_md_config* cfg, double* d_energies);
 
+/* ---- tracing and the collective ledger (trace.hpp, decomp.hpp:64-107) -------------- */
+/* Span (trace.hpp:25-31): phase ids in nnmd::Phase order -- 0 classical_md,
+ * 1 gather_positions, 2 dd_build, 3 neighbor_build, 4 inference, 5 ghost_force_route,
+ * 6 reduce_forces, 7 integrate; rank -1 = step-global phase; seconds on the host steady
+ * clock (TraceSink::now), device intervals measured with CUDA events. */
+typedef struct {
+  int rank;
+  int phase;
+  double t_start, t_end;
+  long step;
+} nnmd_span;
+/* CollectiveRecord (decomp.hpp:84-89): kind 0 gather_positions, 1 ghost_force_route,
+ * 2 reduce_forces; bytes by the reference PayloadLayout (20 B/atom gather, 12 B/atom
+ * reduction, 20 B per routed ghost entry). */
+typedef struct {
+  long step;
+  int kind;
+  uint64_t bytes;
+  int participants;
+} nnmd_collective_record;
+
+/* Record spans and/or ledger entries on subsequent computes (off by default). */
+void nnmd_b200_set_trace(nnmd_b200* ctx, int spans, int ledger);
+/* Step index stamped on the records (StepContext::step); run_md advances it itself. */
+void nnmd_b200_set_step(nnmd_b200* ctx, long step);
+/* Copy out up to cap records; return the total number held (call with cap 0 to size). */
+int nnmd_b200_trace_spans(const nnmd_b200* ctx, nnmd_span* out, int cap);
+int nnmd_b200_ledger(const nnmd_b200* ctx, nnmd_collective_record* out, int cap);
+void nnmd_b200_trace_clear(nnmd_b200* ctx);
+/* export_chrome_trace (trace.cpp:64-85) of the held spans. */
+nnmd_status nnmd_b200_export_chrome_trace(const nnmd_b200* ctx, const char* path);
+
 /* Per-rank statistics of the last compute (RankStats, decomp.hpp:133-142):
  * counts = {locals, ghosts, centres, route_entries}; ms = {dd, neighbor, inference, comm}
  * measured with CUDA events on the rank's stream. */

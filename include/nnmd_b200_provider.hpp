@@ -11,6 +11,7 @@
 
 #include <unistd.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -67,7 +68,7 @@ class GpuDpProvider : public ForceProvider {
 
   std::string name() const override { return opts_.decomposed ? "dp_dd_b200" : "dp_single_b200"; }
 
-  ProviderResult evaluate(const AtomSet& atoms, const SimBox& box, StepContext&) override {
+  ProviderResult evaluate(const AtomSet& atoms, const SimBox& box, StepContext& ctx) override {
     idx_.clear();
     pos_.clear();
     sp_.clear();
@@ -91,8 +92,33 @@ class GpuDpProvider : public ForceProvider {
     const double L[3] = {box.lengths.x, box.lengths.y, box.lengths.z};
     const std::uint8_t per[3] = {box.periodic[0], box.periodic[1], box.periodic[2]};
     f_.assign(3 * idx_.size(), 0.0);
+    // the run's TraceSink / CollectiveLedger get the same spans and records the reference
+    // writes (dd_evaluate, decomp.cpp:285-538; single domain: one rank-0 inference span,
+    // engine.cpp:79), measured on the device
+    nnmd_b200_set_trace(ctx_, ctx.trace != nullptr, ctx.ledger != nullptr && opts_.decomposed);
+    nnmd_b200_set_step(ctx_, ctx.step);
     check(nnmd_b200_compute(ctx_, static_cast<std::int64_t>(idx_.size()), pos_.data(), sp_.data(),
                             gid_.data(), L, per, &out.energy, f_.data(), virial_, nullptr));
+    if (ctx.trace) {
+      std::vector<nnmd_span> sp(static_cast<std::size_t>(nnmd_b200_trace_spans(ctx_, nullptr, 0)));
+      nnmd_b200_trace_spans(ctx_, sp.data(), static_cast<int>(sp.size()));
+      if (opts_.decomposed) {
+        for (const auto& s : sp) ctx.trace->record_span(s.rank, static_cast<Phase>(s.phase), s.t_start, s.t_end, s.step);
+      } else if (!sp.empty()) {
+        double t0 = sp.front().t_start, t1 = sp.front().t_end;
+        for (const auto& s : sp) {
+          t0 = std::min(t0, s.t_start);
+          t1 = std::max(t1, s.t_end);
+        }
+        ctx.trace->record_span(0, Phase::inference, t0, t1, ctx.step);
+      }
+    }
+    if (ctx.ledger && opts_.decomposed) {
+      std::vector<nnmd_collective_record> lr(static_cast<std::size_t>(nnmd_b200_ledger(ctx_, nullptr, 0)));
+      nnmd_b200_ledger(ctx_, lr.data(), static_cast<int>(lr.size()));
+      for (const auto& r : lr) ctx.ledger->add(r.step, static_cast<CollectiveKind>(r.kind), r.bytes, r.participants);
+    }
+    nnmd_b200_trace_clear(ctx_);
     for (std::size_t k = 0; k < idx_.size(); ++k)
       out.forces[static_cast<std::size_t>(idx_[k])] = {f_[3 * k], f_[3 * k + 1], f_[3 * k + 2]};
     return out;

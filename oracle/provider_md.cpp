@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <set>
+#include <tuple>
 
 #include "nnmd/engine.hpp"
 #include "nnmd_b200_provider.hpp"
@@ -82,6 +84,38 @@ int main(int argc, char** argv) {
       d = std::min(d, cfg.box.lengths[c] - d);  // wrapped coordinates
       dx = std::max(dx, d);
     }
+  // trace + ledger parity: the same run_md with a TraceSink and a CollectiveLedger for
+  // both providers -> identical ledger records and identical (rank, phase, step) spans
+  TraceSink tr_ref, tr_gpu;
+  CollectiveLedger lg_ref, lg_gpu;
+  {
+    AtomSet b_ref = cfg.atoms, b_gpu = cfg.atoms;
+    MDConfig md3 = md;
+    md3.n_steps = 3;
+    run_md(b_ref, cfg.box, md3, {&ref}, {}, &tr_ref, &lg_ref);
+    run_md(b_gpu, cfg.box, md3, {&gpu}, {}, &tr_gpu, &lg_gpu);
+  }
+  bool ledger_ok = lg_ref.records().size() == lg_gpu.records().size();
+  for (std::size_t i = 0; ledger_ok && i < lg_ref.records().size(); ++i) {
+    const auto& a = lg_ref.records()[i];
+    const auto& b = lg_gpu.records()[i];
+    ledger_ok = a.step == b.step && a.kind == b.kind && a.bytes == b.bytes && a.participants == b.participants;
+  }
+  auto keys = [](const TraceSink& t) {
+    std::multiset<std::tuple<int, int, long>> k;
+    for (const auto& s : t.spans()) k.insert({s.rank, static_cast<int>(s.phase), s.step});
+    return k;
+  };
+  const bool spans_ok = keys(tr_ref) == keys(tr_gpu) && !tr_gpu.spans().empty();
+  export_chrome_trace(tr_gpu.spans(), "/tmp/nnmd_b200_trace.json");
+  const auto parsed = parse_chrome_trace("/tmp/nnmd_b200_trace.json");
+  const PhaseSummary ps = phase_summary(parsed);
+  const bool chrome_ok = parsed.size() == tr_gpu.spans().size() && ps.aggregate_fraction.count(Phase::inference);
+  std::printf(
+      "{\"trace\": {\"ledger_records\": %zu, \"ledger_match\": %s, \"spans\": %zu, \"span_keys_match\": %s, "
+      "\"chrome_roundtrip\": %s, \"inference_fraction\": %.3f}}\n",
+      lg_gpu.records().size(), ledger_ok ? "true" : "false", tr_gpu.spans().size(), spans_ok ? "true" : "false",
+      chrome_ok ? "true" : "false", ps.aggregate_fraction.count(Phase::inference) ? ps.aggregate_fraction.at(Phase::inference) : 0.0);
   std::printf(
       "{\"provider\": \"%s\", \"steps\": %d, \"atoms\": %zu, \"max_rel_energy_diff\": %.3e, "
       "\"max_position_diff\": %.3e, \"e_ref_step0\": %.10f, \"e_gpu_step0\": %.10f, "
@@ -89,7 +123,7 @@ int main(int argc, char** argv) {
       "\"device_loop_potential_diff\": %.3e, \"device_loop_total_rel_diff\": %.3e}\n",
       gpu.name().c_str(), steps, a_ref.size(), de / std::max(escale, 1e-300), dx,
       s_ref.potential_energy[0], s_gpu.potential_energy[0], dev_dx, dev_dv, dev_de, dev_dt);
-  return (de / std::max(escale, 1e-300) < 1e-5 && dx < 1e-6 && dev_dx == 0.0 && dev_dv == 0.0 && dev_de == 0.0 &&
+  return (ledger_ok && spans_ok && chrome_ok && de / std::max(escale, 1e-300) < 1e-5 && dx < 1e-6 && dev_dx == 0.0 && dev_dv == 0.0 && dev_de == 0.0 &&
           dev_dt < 1e-13)
              ? 0
              : 1;

@@ -84,6 +84,20 @@ _u8p = C.POINTER(C.c_uint8)
 _lib = None
 
 
+class _Span(C.Structure):
+    _fields_ = [("rank", C.c_int), ("phase", C.c_int), ("t_start", C.c_double), ("t_end", C.c_double),
+                ("step", C.c_long)]
+
+
+class _Rec(C.Structure):
+    _fields_ = [("step", C.c_long), ("kind", C.c_int), ("bytes", C.c_uint64), ("participants", C.c_int)]
+
+
+PHASES = ("classical_md", "gather_positions", "dd_build", "neighbor_build", "inference", "ghost_force_route",
+          "reduce_forces", "integrate")
+COLLECTIVES = ("gather_positions", "ghost_force_route", "reduce_forces")
+
+
 class _MdCfg(C.Structure):
     _fields_ = [("dt", C.c_double), ("n_steps", C.c_long), ("equil_steps", C.c_long),
                 ("target_temperature", C.c_double), ("rescale_every", C.c_long)]
@@ -117,6 +131,15 @@ def lib():
                                    C.POINTER(_MdCfg), _dp, _dp]
     L.nnmd_b200_run_md_device.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                           C.c_void_p, _dp, _u8p, C.POINTER(_MdCfg), C.c_void_p]
+    L.nnmd_b200_set_trace.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    L.nnmd_b200_set_trace.restype = None
+    L.nnmd_b200_set_step.argtypes = [C.c_void_p, C.c_long]
+    L.nnmd_b200_set_step.restype = None
+    L.nnmd_b200_trace_spans.argtypes = [C.c_void_p, C.POINTER(_Span), C.c_int]
+    L.nnmd_b200_ledger.argtypes = [C.c_void_p, C.POINTER(_Rec), C.c_int]
+    L.nnmd_b200_trace_clear.argtypes = [C.c_void_p]
+    L.nnmd_b200_trace_clear.restype = None
+    L.nnmd_b200_export_chrome_trace.argtypes = [C.c_void_p, C.c_char_p]
     L.nnmd_b200_rank_stats.argtypes = [C.c_void_p, C.c_int, _i64p, _dp]
     L.nnmd_b200_kernel_times.argtypes = [C.c_void_p, C.POINTER(C.c_char_p), _dp, C.c_int]
     L.nnmd_b200_set_debug.argtypes = [C.c_void_p, C.c_int]
@@ -334,6 +357,33 @@ class DeviceEvaluator:
         _check(lib().nnmd_b200_run_md_device(self._h, n, C.c_void_p(d_coords), C.c_void_p(d_vel),
                                              C.c_void_p(d_mass), C.c_void_p(d_types), C.c_void_p(d_gids), _d(box),
                                              per.ctypes.data_as(_u8p), C.byref(cfg), C.c_void_p(d_energies)))
+
+    # ---- TraceSink / CollectiveLedger (trace.hpp, decomp.hpp:64-107)
+    def set_trace(self, spans: bool = True, ledger: bool = True) -> None:
+        lib().nnmd_b200_set_trace(self._h, int(spans), int(ledger))
+
+    def set_step(self, step: int) -> None:
+        lib().nnmd_b200_set_step(self._h, step)
+
+    def trace_spans(self):
+        """[(rank, phase_name, t_start, t_end, step)] recorded since the last clear."""
+        n = lib().nnmd_b200_trace_spans(self._h, None, 0)
+        buf = (_Span * max(n, 1))()
+        lib().nnmd_b200_trace_spans(self._h, buf, n)
+        return [(s.rank, PHASES[s.phase], s.t_start, s.t_end, s.step) for s in buf[:n]]
+
+    def ledger(self):
+        """[(step, kind_name, bytes, participants)] recorded since the last clear."""
+        n = lib().nnmd_b200_ledger(self._h, None, 0)
+        buf = (_Rec * max(n, 1))()
+        lib().nnmd_b200_ledger(self._h, buf, n)
+        return [(r.step, COLLECTIVES[r.kind], int(r.bytes), r.participants) for r in buf[:n]]
+
+    def clear_trace(self) -> None:
+        lib().nnmd_b200_trace_clear(self._h)
+
+    def export_chrome_trace(self, path: str) -> None:
+        _check(lib().nnmd_b200_export_chrome_trace(self._h, path.encode()))
 
     def compute_device(self, n: int, d_coords: int, d_types: int, d_gids: int, box, d_out: int, periodic=None):
         """Device pointers in/out; d_out = [E, W(9), F(3n), ae(n)] float64."""

@@ -163,6 +163,43 @@ nnmd_status nnmd_b200_compute(nnmd_b200* h, int64_t n, const double* coords, con
   });
 }
 
+void nnmd_b200_set_trace(nnmd_b200* h, int spans, int ledger) {
+  if (h && h->ctx) h->ctx->set_trace(spans != 0, ledger != 0);
+}
+
+void nnmd_b200_set_step(nnmd_b200* h, long step) {
+  if (h && h->ctx) h->ctx->set_step(step);
+}
+
+int nnmd_b200_trace_spans(const nnmd_b200* h, nnmd_span* out, int cap) {
+  if (!h || !h->ctx) return 0;
+  const auto& v = h->ctx->spans();
+  for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i)
+    out[i] = nnmd_span{v[static_cast<size_t>(i)].rank, v[static_cast<size_t>(i)].phase, v[static_cast<size_t>(i)].t0,
+                       v[static_cast<size_t>(i)].t1, v[static_cast<size_t>(i)].step};
+  return static_cast<int>(v.size());
+}
+
+int nnmd_b200_ledger(const nnmd_b200* h, nnmd_collective_record* out, int cap) {
+  if (!h || !h->ctx) return 0;
+  const auto& v = h->ctx->ledger();
+  for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i)
+    out[i] = nnmd_collective_record{v[static_cast<size_t>(i)].step, v[static_cast<size_t>(i)].kind,
+                                    v[static_cast<size_t>(i)].bytes, v[static_cast<size_t>(i)].participants};
+  return static_cast<int>(v.size());
+}
+
+void nnmd_b200_trace_clear(nnmd_b200* h) {
+  if (h && h->ctx) h->ctx->clear_trace();
+}
+
+nnmd_status nnmd_b200_export_chrome_trace(const nnmd_b200* h, const char* path) {
+  return guarded([&] {
+    nb::require(h && h->ctx && path, "nnmd_b200_export_chrome_trace: null argument");
+    h->ctx->export_chrome_trace(path);
+  });
+}
+
 static nb::Context::MdConfig md_cfg(const nnmd_md_config* c) {
   nb::require(c != nullptr, "nnmd_b200_run_md: null config");
   return nb::Context::MdConfig{c->dt, c->n_steps, c->equil_steps, c->target_temperature, c->rescale_every};

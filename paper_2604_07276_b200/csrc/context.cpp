@@ -14,6 +14,8 @@
 #include "context.h"
 
 #include <algorithm>
+#include <chrono>
+#include <fstream>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -104,6 +106,13 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   cudaDeviceProp prop;
   CU(cudaGetDeviceProperties(&prop, o.device));
   n_sm_ = prop.multiProcessorCount;
+  // trace epoch: a device event paired with the host steady clock
+  CU(cudaEventCreate(&epoch_ev_));
+  CU(cudaEventCreate(&md_ev_[0]));
+  CU(cudaEventCreate(&md_ev_[1]));
+  CU(cudaEventRecord(epoch_ev_, st_));
+  CU(cudaEventSynchronize(epoch_ev_));
+  epoch_host_ = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
   wh_ = fold_weights(model_);
   weights_.ensure(wh_.blob.size());
   CU(cudaMemcpy(weights_.p, wh_.blob.data(), wh_.blob.size() * sizeof(float), cudaMemcpyHostToDevice));
@@ -133,6 +142,9 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
 Context::~Context() {
   if (comm_) nccl().CommDestroy(comm_);
   for (auto e : pool_) cudaEventDestroy(e);
+  if (epoch_ev_) cudaEventDestroy(epoch_ev_);
+  for (auto e : md_ev_)
+    if (e) cudaEventDestroy(e);
   if (h_counts_) cudaFreeHost(h_counts_);
   if (h_out_) cudaFreeHost(h_out_);
   if (st_) cudaStreamDestroy(st_);
@@ -229,6 +241,12 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   if (use_nccl_) {
     const double comm = ktimes_.back().second;
     for (auto& s : stats_) s.ms[3] += comm;
+  }
+  if (trace_on_ || ledger_on_) {
+    std::vector<int> local;
+    for (int r = 0; r < opts_.n_ranks; ++r)
+      if (r % opts_.world_size == opts_.world_rank) local.push_back(r);
+    record_trace(n, local);
   }
   if (h_counts_[9] != 0x7f7f7f7f || h_counts_[10] != 0x7f7f7f7f) {
     const int atom = std::min(h_counts_[9], h_counts_[10]);
@@ -677,6 +695,79 @@ void Context::compute_host(long n, const double* pos, const int* types, const in
   if (virial) std::memcpy(virial, head + 1, 9 * sizeof(double));
 }
 
+// ---- trace spans and collective ledger ------------------------------------------------
+double Context::ev_time(cudaEvent_t e) const {
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, epoch_ev_, e));
+  return epoch_host_ + 1e-3 * static_cast<double>(ms);
+}
+
+// Spans of the last compute in dd_evaluate's vocabulary (decomp.cpp:285-538): per rank
+// dd_build / neighbor_build / inference; step-global gather_positions (ownership kernel),
+// ghost_force_route (masked: the per-rank force assembly that routes ghost partials to
+// their owners) and reduce_forces (the NCCL all-reduce, or the end of the on-device
+// accumulation with one process).  Ledger bytes follow the reference PayloadLayout.
+void Context::record_trace(long n, const std::vector<int>& local_ranks) {
+  const int R = opts_.n_ranks;
+  const bool masked = opts_.scheme == NNMD_MASKED_REDUCTION;
+  if (trace_on_) {
+    const Timer* owner = nullptr;
+    const Timer* nccl = nullptr;
+    for (const auto& t : timers_) {
+      if (t.name == "owner") owner = &t;
+      if (t.name == "nccl_allreduce") nccl = &t;
+    }
+    if (owner) spans_.push_back({-1, 1, ev_time(owner->a), ev_time(owner->b), step_});
+    double f0 = 1e300, f1 = -1e300;
+    for (const auto& ph : phases_) {
+      const double t0 = ev_time(timers_[ph.t0].a), t1 = ev_time(timers_[ph.t1].b);
+      if (ph.phase < 3) {
+        spans_.push_back({ph.rank, 2 + ph.phase, t0, t1, step_});
+      } else {
+        f0 = std::min(f0, t0);
+        f1 = std::max(f1, t1);
+      }
+    }
+    if (f1 >= f0) {
+      if (masked) spans_.push_back({-1, 5, f0, f1, step_});
+      if (nccl) spans_.push_back({-1, 6, ev_time(nccl->a), ev_time(nccl->b), step_});
+      else spans_.push_back({-1, 6, f1, f1, step_});
+    }
+  }
+  if (ledger_on_) {
+    ledger_.push_back({step_, 0, static_cast<uint64_t>(n) * 20u, R});
+    if (masked) {
+      uint64_t routed = 0;
+      for (int r : local_ranks) routed += static_cast<uint64_t>(stats_[static_cast<size_t>(r)].counts[3]);
+      ledger_.push_back({step_, 1, routed * 20u, R});
+    }
+    ledger_.push_back({step_, 2, static_cast<uint64_t>(n) * 12u, R});
+  }
+}
+
+// export_chrome_trace (trace.cpp:64-85): JSON array of complete events, microseconds from
+// the earliest span, one lane per rank (tid), args.step.
+void Context::export_chrome_trace(const std::string& path) const {
+  static const char* names[8] = {"classical_md", "gather_positions", "dd_build", "neighbor_build",
+                                 "inference", "ghost_force_route", "reduce_forces", "integrate"};
+  double t0 = spans_.empty() ? 0.0 : spans_.front().t0;
+  for (const auto& s : spans_) t0 = std::min(t0, s.t0);
+  std::ofstream os(path, std::ios::trunc);
+  require(os.good(), "export_chrome_trace: cannot open " + path);
+  os << "[";
+  char buf[512];
+  for (size_t i = 0; i < spans_.size(); ++i) {
+    const auto& s = spans_[i];
+    std::snprintf(buf, sizeof buf,
+                  "%s\n {\"name\": \"%s\", \"cat\": \"md\", \"ph\": \"X\", \"ts\": %.3f, \"dur\": %.3f, "
+                  "\"pid\": 0, \"tid\": %d, \"args\": {\"step\": %ld}}",
+                  i ? "," : "", names[s.phase & 7], (s.t0 - t0) * 1e6, (s.t1 - s.t0) * 1e6, s.rank, s.step);
+    os << buf;
+  }
+  os << "\n]\n";
+  require(os.good(), "export_chrome_trace: write failed");
+}
+
 // ---- device-resident MD loop ---------------------------------------------------------
 void Context::run_md(long n, double* d_pos, double* d_vel, const double* d_mass, const int* d_types,
                      const int64_t* d_gid, const double box[3], const uint8_t periodic[3], const MdConfig& cfg,
@@ -714,12 +805,19 @@ void Context::run_md(long n, double* d_pos, double* d_vel, const double* d_mass,
     // so each process integrates its own copy: no position collective is needed)
     compute_device(n, d_pos, d_types, d_gid, box, periodic, out_.p);
     ma.step = static_cast<int>(step);
+    if (trace_on_) CU(cudaEventRecord(md_ev_[0], st_));
     launch_leapfrog(ma, st_);
     launch_energy_record(md_ke_.p, ma.n, out_.p, d_rec, step, st_);
     if (cfg.target_temperature > 0.0 && step < cfg.equil_steps && cfg.rescale_every > 0 &&
         (step + 1) % cfg.rescale_every == 0)
       launch_rescale(ma.n, d_vel, d_mass, md_ke_.p, md_sum_.p, cfg.target_temperature, st_);
     check_launch("md_step");
+    if (trace_on_) {
+      CU(cudaEventRecord(md_ev_[1], st_));
+      CU(cudaEventSynchronize(md_ev_[1]));
+      spans_.push_back({-1, 7, ev_time(md_ev_[0]), ev_time(md_ev_[1]), step_});
+    }
+    ++step_;
   }
   check_forces();
 }

@@ -35,6 +35,24 @@ struct Timer {
   cudaEvent_t a, b;
 };
 
+// Trace span / collective record in the reference's vocabulary (trace.hpp Span, Phase;
+// decomp.hpp CollectiveRecord, CollectiveKind).  Phase ids follow nnmd::Phase order:
+// 0 classical_md, 1 gather_positions, 2 dd_build, 3 neighbor_build, 4 inference,
+// 5 ghost_force_route, 6 reduce_forces, 7 integrate.  Kinds: 0 gather_positions,
+// 1 ghost_force_route, 2 reduce_forces.
+struct TraceSpan {
+  int rank;  // -1: step-global phase
+  int phase;
+  double t0, t1;  // seconds on the host steady clock (device times from CUDA events)
+  long step;
+};
+struct LedgerRec {
+  long step;
+  int kind;
+  uint64_t bytes;
+  int participants;
+};
+
 class Context {
  public:
   Context(const Model& m, const nnmd_b200_opts& o);
@@ -64,6 +82,22 @@ class Context {
   void run_md_host(long n, double* pos, double* vel, const double* mass, const int* types, const int64_t* gid,
                    const double box[3], const uint8_t periodic[3], const MdConfig& cfg, double* potential,
                    double* total);
+
+  // Tracing (TraceSink spans from CUDA events) and the collective ledger
+  // (CollectiveLedger with the reference PayloadLayout: 20 B/atom gather, 12 B/atom
+  // reduction, 20 B per routed ghost entry).  Records accumulate until clear_trace().
+  void set_trace(bool spans, bool ledger) {
+    trace_on_ = spans;
+    ledger_on_ = ledger;
+  }
+  void set_step(long step) { step_ = step; }
+  const std::vector<TraceSpan>& spans() const { return spans_; }
+  const std::vector<LedgerRec>& ledger() const { return ledger_; }
+  void clear_trace() {
+    spans_.clear();
+    ledger_.clear();
+  }
+  void export_chrome_trace(const std::string& path) const;
 
   cudaStream_t stream() const { return st_; }
   const RankStat& stat(int r) const { return stats_.at(static_cast<size_t>(r)); }
@@ -122,6 +156,16 @@ class Context {
   };
   std::vector<PhaseMark> phases_;
   int keep_debug_ = 0;
+  // trace / ledger
+  bool trace_on_ = false, ledger_on_ = false;
+  long step_ = 0;
+  cudaEvent_t epoch_ev_ = nullptr;
+  double epoch_host_ = 0.0;
+  std::vector<TraceSpan> spans_;
+  std::vector<LedgerRec> ledger_;
+  double ev_time(cudaEvent_t e) const;
+  void record_trace(long n, const std::vector<int>& local_ranks);
+  cudaEvent_t md_ev_[2] = {nullptr, nullptr};
   // pinned host staging for the host API
   double* h_out_ = nullptr;
   size_t h_out_cap_ = 0;
