@@ -28,7 +28,7 @@ namespace nb {
 namespace {
 
 struct Slot {
-  float *T, *Qb, *DX0, *DX1, *dU;
+  float *T, *DX0, *DX1, *dU;
 };
 
 __host__ __device__ inline int max_width(const DpArgs& a) {
@@ -53,7 +53,6 @@ __device__ inline Slot slot_of(const DpArgs& a, float* base, int n) {
   Slot s;
   size_t o = 0;
   s.T = base + o;   o += nm * nm4;
-  s.Qb = base + o;  o += nm * nm4;
   s.DX0 = base + o; o += align4(nm * W);
   s.DX1 = base + o; o += align4(nm * W);
   s.dU = base + o;  o += align4(nm * M2);
@@ -109,6 +108,10 @@ struct Mm {
 __host__ __device__ inline size_t head_bytes(int mode, int nst = 1) {
   return mode == 0 ? sizeof(GemmSmem) : (nst == 1 ? sizeof(tc::Smem<1>) : sizeof(tc::Smem<2>));
 }
+
+// Column-pass partials inside the tcgen05 operand-stage buffer, behind the epilogue's
+// 128 x 132-float staging tile (67,584 bytes) when that pass runs in the T-GEMM epilogue.
+constexpr size_t kPartOff = 69632;
 
 struct Smem {
   unsigned char* head;
@@ -286,12 +289,14 @@ __device__ void softmax_gate(int n, int ln, const float* S, int lds, float* PU, 
   }
 }
 
-// Backward row pass (warp per query row k, float4 over key columns j):
-//   dP = dP~ Theta, dC = dP~ P / sigma  ->  DP, DC (ld ln)
-//   t_k = sum_j dP P,  dsigma partial -sum_j dC C / sigma,  dR_k += sum_j dC_kj R_j
-// TS: dP~ (ld ldt; the T-GEMM's shared-memory accumulator tile, or DP itself).
-__device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const float* __restrict__ PU, float* DP,
-                             float* __restrict__ DC, float inv_sig, const Smem& sm) {
+// Backward of one gated attention layer's n x n part, from dP~ = dY U_B^T (TS, ld ldt:
+// the T-GEMM's shared-memory accumulator tile, or a global copy) and the stashed softmax
+// weights pu (PU, ld ln).  With C = R R^T, Theta = C / sigma, P = s_j^2 pu:
+//   dP = dP~ Theta,  dC = dP~ P / sigma,  t_k = sum_j dP P
+// Row pass (warp per query row k, float4 over j): t_k, the dsigma partial
+// -sum_j dC C / sigma, and the row half of the gate term dR_k += sum_j dC_kj R_j.
+__device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const float* __restrict__ PU, float inv_sig,
+                             const Smem& sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = wid; k < n; k += nw) {
     const float4 Rk = sm.R[k];
@@ -301,12 +306,9 @@ __device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const floa
       const float4 pu = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(k) * ln + j4);
       const float tq[4] = {tv.x, tv.y, tv.z, tv.w};
       const float pq[4] = {pu.x, pu.y, pu.z, pu.w};
-      float dpo[4], dco[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int j = j4 + q;
-        dpo[q] = 0.f;
-        dco[q] = 0.f;
         if (j < n) {
           const float sj = sm.s[j];
           const float4 Rj = sm.R[j];
@@ -314,8 +316,6 @@ __device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const floa
           const float pv = sj * sj * pq[q];
           const float dP = tq[q] * C * inv_sig;
           const float dC = tq[q] * pv * inv_sig;
-          dpo[q] = dP;
-          dco[q] = dC;
           dsg -= dC * C * inv_sig;
           t += dP * pv;
           g0 += dC * Rj.x;
@@ -324,9 +324,6 @@ __device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const floa
           g3 += dC * Rj.w;
         }
       }
-      const size_t kj = static_cast<size_t>(k) * ln + j4;
-      *reinterpret_cast<float4*>(DP + kj) = make_float4(dpo[0], dpo[1], dpo[2], dpo[3]);
-      *reinterpret_cast<float4*>(DC + kj) = make_float4(dco[0], dco[1], dco[2], dco[3]);
     }
     t = warp_sum(t);
     dsg = warp_sum(dsg);
@@ -347,11 +344,68 @@ __device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const floa
   }
 }
 
+// Column pass (thread per key column j and k-half, coalesced across threads), after the
+// row pass: dP and dC recomputed from dP~, dw_j of the s_j^2 softmax weights, the column
+// half of the gate term dR_j += sum_k dC_kj R_k, dsx_j += 2 s_j (dw_j + dsigma), and
+// dS = P o (dP - t) written to DS (ld ln; may alias TS when ldt == ln).
+// part: [2][stride] float4 + [2][stride] float of shared memory (stride >= n).
+__device__ void bwd_col_pass(int n, int ln, int stride, const float* TS, int ldt, const float* __restrict__ PU,
+                             float* DS, float inv_sig, const Smem& sm, unsigned char* part_raw) {
+  const int nh = (n + 1) >> 1;
+  const int half_threads = blockDim.x >> 1;
+  float4* part = reinterpret_cast<float4*>(part_raw);   // [2][stride] (g0..g3)
+  float* partw = reinterpret_cast<float*>(part + 2 * stride);  // [2][stride]
+  const int h = threadIdx.x / half_threads;
+  for (int j = threadIdx.x - h * half_threads; j < n; j += half_threads) {
+    float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+    const float sj = sm.s[j];
+    const float sj2 = sj * sj;
+    const float4 Rj = sm.R[j];
+    const int kb = h * nh, ke = min(n, kb + nh);
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      const float pu = PU[static_cast<size_t>(k) * ln + j];
+      const float tv = TS[static_cast<size_t>(k) * ldt + j];
+      const float4 Rk = sm.R[k];
+      const float C = dot4(Rk, Rj);
+      const float dP = tv * C * inv_sig;
+      const float dC = tv * (sj2 * pu) * inv_sig;
+      const float dpt = dP - sm.t[k];
+      dw += pu * dpt;
+      DS[static_cast<size_t>(k) * ln + j] = sj2 * pu * dpt;
+      g0 += dC * Rk.x;
+      g1 += dC * Rk.y;
+      g2 += dC * Rk.z;
+      g3 += dC * Rk.w;
+    }
+    part[h * stride + j] = make_float4(g0, g1, g2, g3);
+    partw[h * stride + j] = dw;
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    float ds = 0.f;
+    for (int k = 0; k < n; ++k) ds += sm.rowpart[k];
+    sm.red[0] = ds;
+  }
+  __syncthreads();
+  const float dsig = static_cast<float>(sm.red[0]);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const float4 p0 = part[j], p1 = part[stride + j];
+    const float dw = partw[j] + partw[stride + j];
+    sm.dsx[j] += 2.f * sm.s[j] * (dw + dsig);
+    float4 r = sm.dR[j];
+    r.x += p0.x + p1.x;
+    r.y += p0.y + p1.y;
+    r.z += p0.z + p1.z;
+    r.w += p0.w + p1.w;
+    sm.dR[j] = r;
+  }
+}
+
 }  // namespace
 
 size_t dp_scratch_floats(const DpArgs& a) {
   const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a);
-  return align4(nm * M2) + nm * align4(nm) * 2 + align4(nm * W) * 2 + 64;
+  return align4(nm * M2) + nm * align4(nm) + align4(nm * W) * 2 + 64;
 }
 
 size_t dp_smem_bytes(const DpArgs& a, int mode) { return smem_layout(a, mode, nullptr, nullptr) + 1024; }
@@ -588,77 +642,31 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         else prefetch_l2(a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, sizeof(float) * a.emb_centre_stride);
       }
       pc.mark(2);
-      // T = dP~ = dY U_B^T, then the row pass (warp per query row k): dP = dP~ Theta,
-      // dC = dP~ P / sigma, t_k = sum_j dP P, dsigma partials, and the row half of the
-      // gate term dR_k += sum_j dC_kj R_j.  With tcgen05 and n <= 128 the row pass runs
-      // in the GEMM epilogue on the shared-memory accumulator tile.
-      bool fused_row = false;
+      // T = dP~ = dY U_B^T, then the row and column passes (bwd_row_pass, bwd_col_pass)
+      // -> dS in sl.T.  With tcgen05 and n <= 128 both passes run in the GEMM epilogue on
+      // the shared-memory accumulator tile (dP~ never goes to global memory); the column
+      // partials sit behind that tile in the same (idle) operand-stage buffer.
+      bool fused_rc = false;
       if constexpr (MODE != 0) {
         if (n <= 128 && !(a.flags & 2)) {
+          unsigned char* part = sm.head + kPartOff;
           mm.template run<false, true, 0, 2>(n, n, M, dY, M, Ul + M, M2,
                                              [&](const float* stg, int ldst, int, int, int, int) {
-                                               bwd_row_pass(n, ln, stg, ldst, PUl, sl.T, sl.Qb, inv_sig, sm);
+                                               bwd_row_pass(n, ln, stg, ldst, PUl, inv_sig, sm);
+                                               __syncthreads();
+                                               bwd_col_pass(n, ln, n, stg, ldst, PUl, sl.T, inv_sig, sm, part);
                                              });
-          fused_row = true;
+          fused_rc = true;
         }
       }
-      if (!fused_row) {
+      if (!fused_rc) {
         mm.template run<false, true>(n, n, M, dY, M, Ul + M, M2,
                                      [&](int k, int j, auto v) { vst(&sl.T[k * ln + j], v); });
         __syncthreads();
         pc.mark(5);
-        bwd_row_pass(n, ln, sl.T, ln, PUl, sl.T, sl.Qb, inv_sig, sm);
-      }
-      __syncthreads();
-      pc.mark(6);
-      // column pass (thread per key column j and k-half, coalesced across threads): dw_j
-      // of the s_j^2 softmax weights, the column half of the gate term
-      // dR_j += sum_k dC_kj R_k, and dS = P o (dP - t) written in place over dP.
-      {
-        const int nh = (n + 1) >> 1;
-        const int half_threads = blockDim.x >> 1;
-        float4* part = reinterpret_cast<float4*>(sm.part);          // [2][n] (g0..g3)
-        float* partw = reinterpret_cast<float*>(part + 2 * a.n_max);   // [2][n]
-        const int h = threadIdx.x / half_threads;
-        for (int j = threadIdx.x - h * half_threads; j < n; j += half_threads) {
-          float dw = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
-          const float sj2 = sm.s[j] * sm.s[j];
-          const int kb = h * nh, ke = min(n, kb + nh);
-#pragma unroll 4
-          for (int k = kb; k < ke; ++k) {
-            const size_t kj = static_cast<size_t>(k) * ln + j;
-            const float pu = PUl[kj];
-            const float dpt = sl.T[kj] - sm.t[k];
-            dw += pu * dpt;
-            sl.T[kj] = sj2 * pu * dpt;
-            const float dC = sl.Qb[kj];
-            const float4 Rk = sm.R[k];
-            g0 += dC * Rk.x;
-            g1 += dC * Rk.y;
-            g2 += dC * Rk.z;
-            g3 += dC * Rk.w;
-          }
-          part[h * a.n_max + j] = make_float4(g0, g1, g2, g3);
-          partw[h * a.n_max + j] = dw;
-        }
-        if (threadIdx.x == blockDim.x - 1) {
-          float ds = 0.f;
-          for (int k = 0; k < n; ++k) ds += sm.rowpart[k];
-          sm.red[0] = ds;
-        }
+        bwd_row_pass(n, ln, sl.T, ln, PUl, inv_sig, sm);
         __syncthreads();
-        const float dsig = static_cast<float>(sm.red[0]);
-        for (int j = threadIdx.x; j < n; j += blockDim.x) {
-          const float4 p0 = part[j], p1 = part[a.n_max + j];
-          const float dw = partw[j] + partw[a.n_max + j];
-          sm.dsx[j] += 2.f * sm.s[j] * (dw + dsig);
-          float4 r = sm.dR[j];
-          r.x += p0.x + p1.x;
-          r.y += p0.y + p1.y;
-          r.z += p0.z + p1.z;
-          r.w += p0.w + p1.w;
-          sm.dR[j] = r;
-        }
+        bwd_col_pass(n, ln, n, sl.T, ln, PUl, sl.T, inv_sig, sm, sm.part);
       }
       __syncthreads();
       pc.mark(7);

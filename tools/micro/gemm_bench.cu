@@ -1,34 +1,30 @@
-// Microbenchmark of the per-centre block GEMM (tc_gemm.cuh): G back-to-back GEMMs per
-// CTA on L2-resident operands, 2 CTAs per SM (production smem footprint), all SMs.
-// Build+run on the GPU box:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
-//   -I paper_2604_07276_b200/csrc tools/micro/gemm_bench.cu -o /tmp/gb && /tmp/gb
+// Microbenchmark of the per-centre block GEMMs (tc_gemm.cuh): G back-to-back GEMMs per CTA
+// on L2-resident operands, production smem footprint (2 CTAs per SM), cycles from clock64.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr
+//        -I paper_2604_07276_b200/csrc tools/micro/gemm_bench.cu -o /tmp/gb && /tmp/gb
+// dbg bits: 1 skip operand loads, 2 skip MMA issue, 4 skip epilogue.
 #include <cstdio>
-#include <vector>
 #include "tc_gemm.cuh"
 
 using namespace nb;
 
-template <bool TA, bool TB, int NPASS, int NST = 2, int KC = 16>
-__global__ void __launch_bounds__(256, 2) kbench(int M, int N, int K, int G, const float* A, const float* B,
-                                                  float* C, size_t slot, int dbg, long long* cyc,
-                                                  unsigned long long* prof) {
+template <bool TS, bool TA, bool TB, int NPASS>
+__global__ void __launch_bounds__(256, 2) kbench(int M, int N, int K, int G, const float* A, const float* B, float* C,
+                                                  size_t slot, int dbg, long long* cyc) {
   extern __shared__ __align__(1024) unsigned char raw[];
   unsigned char* head = raw + ((1024 - (tc::smem_u32(raw) & 1023)) & 1023);
   tc::State st;
-  tc::init(st, reinterpret_cast<tc::Smem<NST, KC>*>(head), 256);
+  tc::init(st, reinterpret_cast<tc::Smem<1>*>(head), 256);
   st.dbg = dbg;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st.prof = prof;
-    st.t_last = clock64();
-  }
   const float* a = A + blockIdx.x * slot;
   const float* b = B + blockIdx.x * slot;
   float* c = C + blockIdx.x * slot;
   const int lda = TA ? M : K, ldb = TB ? K : N;
   const long long t0 = clock64();
   for (int g = 0; g < G; ++g) {
-    tc::gemm<TA, TB, NPASS, 0, NST, KC, 1>(st, M, N, K, a, lda, b, ldb,
-                                     [&](int m, int n, auto v) { vst(&c[m * N + n], v); });
+    auto epi = [&](int m, int n, auto v) { vst(&c[m * N + n], v); };
+    if (TS) tc::gemm_ts<TA, TB, NPASS, 1>(st, M, N, K, a, lda, b, ldb, epi);
+    else tc::gemm<TA, TB, NPASS, 0, 1, 1>(st, M, N, K, a, lda, b, ldb, epi);
     __syncthreads();
   }
   if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = clock64() - t0;
@@ -41,40 +37,24 @@ __global__ void kspin(long long n) {
   }
 }
 
-template <bool TA, bool TB, int NPASS, int NST = 2, int KC = 16>
+template <bool TS, bool TA, bool TB, int NPASS>
 void run(int M, int N, int K, float* A, float* B, float* C, size_t slot, int grid, int dbg = 0) {
-  const size_t smem = sizeof(tc::Smem<NST, KC>) + 1024 + 8192;  // + the production kernels' extra smem
-  auto k = kbench<TA, TB, NPASS, NST, KC>;
+  const size_t smem = sizeof(tc::Smem<1>) + 1024 + 8192;  // + the production kernels' extra smem
+  auto k = kbench<TS, TA, TB, NPASS>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int G = 64;
   static long long* cyc = nullptr;
-  static unsigned long long* prof = nullptr;
   if (!cyc) cudaMallocManaged(&cyc, 8);
-  if (!prof) cudaMallocManaged(&prof, 64);
-  kspin<<<148, 32>>>(400000000LL);  // ~200 ms at boost: clocks up before timing
-  k<<<grid, 256, smem>>>(M, N, K, 2, A, B, C, slot, dbg, cyc, prof);
+  const int G = 64;
+  kspin<<<148, 32>>>(200000000LL);
+  k<<<grid, 256, smem>>>(M, N, K, 2, A, B, C, slot, dbg, cyc);
+  k<<<grid, 256, smem>>>(M, N, K, G, A, B, C, slot, dbg, cyc);
   cudaDeviceSynchronize();
-  for (int i = 0; i < 8; ++i) prof[i] = 0;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventRecord(e0);
-  k<<<grid, 256, smem>>>(M, N, K, G, A, B, C, slot, dbg, cyc, prof);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  float ms;
-  cudaEventElapsedTime(&ms, e0, e1);
-  const double per = ms * 1e3 / G;  // us per GEMM (per CTA, all CTAs concurrently)
-  cudaDeviceSynchronize();
-  const double clk = double(*cyc) / G;  // SM cycles per GEMM (block 0, clock64)
+  const double clk = double(*cyc) / G;
   const double mac = double(M) * N * K * NPASS;
-  printf("NST=%d KC=%d dbg=%d grid=%d TA=%d TB=%d NPASS=%d M=%d N=%d K=%d: %.2f us/GEMM/CTA = %.0f clk; SM-level %.0f clk per GEMM-pair;"
-         " tensor util %.1f%% (1024 tf32 MAC/clk/SM)  err=%s\n",
-         NST, KC, dbg, grid, TA, TB, NPASS, M, N, K, per, clk, clk, 100.0 * 2 * mac / 1024.0 / clk,
+  printf("%s dbg=%d grid=%3d TA=%d TB=%d NPASS=%d M=%d N=%3d K=%3d: %6.0f clk/GEMM/CTA  tensor %.0f%% of 2048 MAC/clk "
+         "per SM  err=%s\n",
+         TS ? "TS" : "SS", dbg, grid, TA, TB, NPASS, M, N, K, clk, 100.0 * (grid > 148 ? 2 : 1) * mac / 2048.0 / clk,
          cudaGetErrorString(cudaGetLastError()));
-  printf("   ticks/GEMM:");
-  for (int i = 0; i < 8; ++i) printf(" g%d=%.0f", i, double(prof[i]) / G);
-  printf("\n");
 }
 
 int main() {
@@ -86,19 +66,17 @@ int main() {
   cudaMalloc(&C, grid * slot * 4);
   cudaMemset(A, 0, grid * slot * 4);
   cudaMemset(B, 0, grid * slot * 4);
-  struct S { int M, N, K; } shapes[] = {{128, 128, 128}, {128, 256, 128}, {128, 96, 128}, {128, 128, 96}, {128, 128, 256}};
-  for (int dbg : {0, 7, 31}) {
-    for (int K : {128}) {
-      run<false, true, 3>(128, 128, K, A, B, C, slot, 1, dbg);
-      run<false, true, 3, 1, 32>(128, 128, K, A, B, C, slot, 1, dbg);
-    }
+  for (int dbg : {0, 1, 4, 5, 7, 3}) {
+    run<true, false, true, 3>(128, 128, 128, A, B, C, slot, 1, dbg);
+    run<false, false, true, 3>(128, 128, 128, A, B, C, slot, 1, dbg);
   }
+  struct S { int M, N, K; } shapes[] = {{128, 128, 128}, {128, 96, 128}, {128, 128, 96}, {128, 128, 256}};
   for (auto s : shapes) {
-    run<false, false, 3, 1, 32>(s.M, s.N, s.K, A, B, C, slot, grid);
-    run<false, false, 3>(s.M, s.N, s.K, A, B, C, slot, grid);
-    run<false, false, 1>(s.M, s.N, s.K, A, B, C, slot, grid);
-    run<true, false, 3>(s.M, s.N, s.K, A, B, C, slot, grid);
-    run<false, true, 3>(s.M, s.N, s.K, A, B, C, slot, grid);
+    run<false, false, false, 3>(s.M, s.N, s.K, A, B, C, slot, grid);
+    run<true, false, false, 3>(s.M, s.N, s.K, A, B, C, slot, grid);
+    run<true, true, false, 3>(s.M, s.N, s.K, A, B, C, slot, grid);
+    run<true, false, true, 3>(s.M, s.N, s.K, A, B, C, slot, grid);
+    run<true, false, false, 1>(s.M, s.N, s.K, A, B, C, slot, grid);
   }
   return 0;
 }
