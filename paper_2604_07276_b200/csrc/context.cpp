@@ -58,6 +58,7 @@ template struct DevBuf<float>;
 template struct DevBuf<float4>;
 template struct DevBuf<double>;
 template struct DevBuf<int64_t>;
+template struct DevBuf<uint8_t>;
 template struct DevBuf<unsigned long long>;
 
 // partition_ranks (decomp.cpp:17-57): minimise subdomain surface; ties -> most balanced
@@ -116,6 +117,7 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   wh_ = fold_weights(model_);
   weights_.ensure(wh_.blob.size());
   CU(cudaMemcpy(weights_.p, wh_.blob.data(), wh_.blob.size() * sizeof(float), cudaMemcpyHostToDevice));
+  build_weight_images();
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_counts_), 64 * sizeof(int)));
   require(o.n_ranks <= 48, "nnmd_b200: at most 48 DD ranks");
   stats_.resize(static_cast<size_t>(o.n_ranks));
@@ -483,6 +485,21 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.vir = vir_.p;
   static const int flags = getenv("NNMD_FLAGS") ? atoi(getenv("NNMD_FLAGS")) : 0;
   dp.flags = flags;
+  if (!(flags & 4) && wimg_.p) {  // bit 2: stage weights through registers instead
+    auto img = [&](long off) -> const uint8_t* { return off >= 0 ? wimg_.p + off : nullptr; };
+    for (int l = 0; l < m.na; ++l) {
+      dp.img_ab[l] = img(wimg_ab_[static_cast<size_t>(l)]);
+      dp.img_abT[l] = img(wimg_abT_[static_cast<size_t>(l)]);
+    }
+    bool all = true;
+    for (int l = 0; l < m.na; ++l) all = all && dp.img_ab[l] && dp.img_abT[l];
+    for (int e = 1; e < dp.n_embed; ++e) {
+      dp.img_ew[e] = img(wimg_ew_[static_cast<size_t>(e)]);
+      dp.img_ewT[e] = img(wimg_ewT_[static_cast<size_t>(e)]);
+      all = all && dp.img_ew[e] && dp.img_ewT[e];
+    }
+    dp.wimg = all ? 1 : 0;
+  }
   dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
   const int grid = std::max(1, std::min(ncen, 2 * n_sm_));  // two CTAs per SM (SIMT and tcgen05)
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
@@ -693,6 +710,47 @@ void Context::compute_host(long n, const double* pos, const int* types, const in
   CU(cudaStreamSynchronize(st_));
   if (energy) *energy = head[0];
   if (virial) std::memcpy(virial, head + 1, 9 * sizeof(double));
+}
+
+// ---- pre-split weight images -----------------------------------------------------------
+// B operands of the per-centre weight GEMMs (dp_kernels.cu): U = X [A|B] (K = M, N = 2M),
+// dX += dU [A|B]^T (K = 2M, N = M), embedding forward (K = E_in, N = E_out) and backward
+// (K = E_out, N = E_in).  Only operands that fit one MMA tile (N <= 256) get an image.
+void Context::build_weight_images() {
+  const int M = model_.M, M2 = 2 * M;
+  const int ne = static_cast<int>(wh_.edims.size());
+  struct Job {
+    long* slot;
+    long w;
+    int tb, ldb, K, N;
+  };
+  std::vector<Job> jobs;
+  wimg_ab_.assign(static_cast<size_t>(model_.na), -1);
+  wimg_abT_.assign(static_cast<size_t>(model_.na), -1);
+  wimg_ew_.assign(static_cast<size_t>(ne), -1);
+  wimg_ewT_.assign(static_cast<size_t>(ne), -1);
+  for (int l = 0; l < model_.na; ++l) {
+    jobs.push_back({&wimg_ab_[static_cast<size_t>(l)], wh_.ab[static_cast<size_t>(l)], 0, M2, M, M2});
+    jobs.push_back({&wimg_abT_[static_cast<size_t>(l)], wh_.ab[static_cast<size_t>(l)], 1, M2, M2, M});
+  }
+  for (int e = 1; e < ne; ++e) {
+    const int Ein = wh_.edims[static_cast<size_t>(e - 1)], Eout = wh_.edims[static_cast<size_t>(e)];
+    jobs.push_back({&wimg_ew_[static_cast<size_t>(e)], wh_.ew[static_cast<size_t>(e)], 1, Ein, Ein, Eout});
+    jobs.push_back({&wimg_ewT_[static_cast<size_t>(e)], wh_.ew[static_cast<size_t>(e)], 0, Ein, Eout, Ein});
+  }
+  size_t total = 0;
+  for (auto& j : jobs) {
+    // one MMA tile per image: the SS path (N > 128) covers N <= 256, the TS path N <= 128
+    if (j.N > 256) continue;
+    *j.slot = static_cast<long>(total);
+    total += (weight_image_bytes(j.K, j.N) + 1023) & ~size_t(1023);
+  }
+  if (total == 0) return;
+  wimg_.ensure(total);
+  for (auto& j : jobs)
+    if (*j.slot >= 0) launch_weight_image(weights_.p + j.w, j.tb, j.ldb, j.K, j.N, wimg_.p + *j.slot, st_);
+  check_launch("weight_image");
+  CU(cudaStreamSynchronize(st_));
 }
 
 // ---- trace spans and collective ledger ------------------------------------------------

@@ -119,6 +119,10 @@ class Context {
   int n_sm_ = 148;
 
   DevBuf<float> weights_;
+  // pre-split weight images (launch_weight_image), byte offsets into wimg_ (-1: none)
+  DevBuf<uint8_t> wimg_;
+  std::vector<long> wimg_ab_, wimg_abT_, wimg_ew_, wimg_ewT_;
+  void build_weight_images();
   NcclComm comm_ = nullptr;
   bool use_nccl_ = false;
 

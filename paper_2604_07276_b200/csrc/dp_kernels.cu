@@ -17,6 +17,7 @@
 //   dP~ = dY U_B^T, dU_B = P~^T dY, dS = P o (dP - t), dU_A = dS X,
 //   dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T
 #include <cfloat>
+#include <type_traits>
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
@@ -74,31 +75,34 @@ struct Mm {
   __device__ void finish() {
     if constexpr (MODE != 0) tc::finish(st);
   }
-  template <bool TA, bool TB, int PROMOTE = 0, int EK = 1, class Epi>
+  // img: optional pre-split image of the weight operand B (DpArgs::img_*), N <= 256.
+  template <bool TA, bool TB, int PROMOTE = 0, int EK = 1, bool IMG = false, class Epi>
   __device__ __forceinline__ void run(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
-                                      Epi epi) {
+                                      Epi epi, const uint8_t* img = nullptr) {
     if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
     else if constexpr (NST == 1 && PROMOTE == 0) {
       // N > 128 would need a second A staging per 128-column tile in TS mode: the wide
       // U = X [A|B] product stays on the SS path, which covers N = 256 in one tile
-      if (N <= tc::kTsN) tc::gemm_ts<TA, TB, MODE == 1 ? 3 : 1, EK>(st, M, N, K, A, lda, B, ldb, epi);
-      else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, 0, 1, EK>(st, M, N, K, A, lda, B, ldb, epi);
+      if (N <= tc::kTsN) tc::gemm_ts<TA, TB, MODE == 1 ? 3 : 1, EK, IMG>(st, M, N, K, A, lda, B, ldb, epi, img);
+      else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, 0, 1, EK, IMG>(st, M, N, K, A, lda, B, ldb, epi, img);
     } else {
       tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
     }
   }
   // C = epi(A1 B1 + A2 B2) with one accumulator (tcgen05) or, on the SIMT path, two
   // passes through `acc` (ld N, must not alias the epilogue's sources).
-  template <bool TA, bool TB, bool TA2, bool TB2, class Epi>
+  template <bool TA, bool TB, bool TA2, bool TB2, bool IMG2 = false, class Epi>
   __device__ __forceinline__ void run2(int M, int N, int K, const float* A, int lda, const float* B, int ldb, int K2,
-                                       const float* A2, int lda2, const float* B2, int ldb2, float* acc, Epi epi) {
+                                       const float* A2, int lda2, const float* B2, int ldb2, float* acc, Epi epi,
+                                       const uint8_t* img2 = nullptr) {
     if constexpr (MODE == 0) {
       bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, [&](int m, int n, float v) { acc[m * N + n] = v; });
       __syncthreads();
       bgemm<TA2, TB2>(M, N, K2, A2, lda2, B2, ldb2, *gs, [&](int m, int n, float v) { epi(m, n, acc[m * N + n] + v); });
     } else {
       if constexpr (NST == 1)
-        tc::gemm2_ts<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 1>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
+        tc::gemm2_ts<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 1, false, IMG2>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2,
+                                                                          B2, ldb2, epi, nullptr, img2);
       else
         tc::gemm2<TA, TB, TA2, TB2, MODE == 1 ? 3 : 1, 0, NST, 1>(st, M, N, K, A, lda, B, ldb, K2, A2, lda2, B2, ldb2, epi);
     }
@@ -205,7 +209,7 @@ __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int
 
 // Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
 // Writes intermediate activations to EMB and the last to `out` (n x M).
-template <int MODE>
+template <int MODE, bool WIMG>
 __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, const Smem& sm, float* emb,
                               float* out) {
   const int E0 = a.edims[0];
@@ -221,8 +225,9 @@ __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, c
     const int Ein = a.edims[e - 1], Eout = a.edims[e];
     float* nxt = (e + 1 == a.n_embed) ? out : emb + off;
     const float* b = a.eb[e];
-    mm.template run<false, true>(n, Eout, Ein, cur, Ein, a.ew[e], Ein,
-                                 [&](int m, int o, auto v) { vst(&nxt[m * Eout + o], vtanh(v + vld(&b[o], v))); });
+    mm.template run<false, true, 0, 1, WIMG>(n, Eout, Ein, cur, Ein, a.ew[e], Ein,
+                                             [&](int m, int o, auto v) { vst(&nxt[m * Eout + o], vtanh(v + vld(&b[o], v))); },
+                                             a.img_ew[e]);
     __syncthreads();
     cur = nxt;
     off += static_cast<size_t>(a.n_max) * Eout;
@@ -413,7 +418,7 @@ size_t dp_smem_bytes(const DpArgs& a, int mode) { return smem_layout(a, mode, nu
 // ------------------------------------------------------------------------------------
 // Forward: rows -> embedding -> attention layers -> descriptor D = (X^T R)(R^T X_<) / n_max
 // ------------------------------------------------------------------------------------
-template <int MODE>
+template <int MODE, bool WIMG>
 __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant__ DpArgs a) {
   extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
@@ -438,7 +443,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
     pc.mark(0);
     const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
     float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
-    embed_forward(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, X);
+    embed_forward<MODE, WIMG>(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, X);
     pc.mark(1);
     for (int l = 0; l < a.n_attn; ++l) {
       const float* Xl = X + l * a.x_layer_stride;
@@ -446,8 +451,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
       float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
       float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
       float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
-      mm.template run<false, false>(n, M2, M, Xl, M, a.ab[l], M2,
-                          [&](int k, int j, auto v) { vst(&Ul[k * M2 + j], v); });
+      mm.template run<false, false, 0, 1, WIMG>(n, M2, M, Xl, M, a.ab[l], M2,
+                                                [&](int k, int j, auto v) { vst(&Ul[k * M2 + j], v); }, a.img_ab[l]);
       __syncthreads();
       pc.mark(2);
       bool fused_softmax = false;
@@ -516,7 +521,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
 // Backward: dD -> (dA, dB) -> dX, dR -> attention layers in reverse -> embedding ->
 // row gradients g_k = de/dd_k (FP64 geometry), per-centre virial -sum g (x) d.
 // ------------------------------------------------------------------------------------
-template <int MODE>
+template <int MODE, bool WIMG>
 __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constant__ DpArgs a) {
   extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
@@ -682,16 +687,18 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         float* xo = dXn;
         const float* yi = dY;
         if (l > 0) {
-          mm.template run2<true, false, false, true>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
-                                                     [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&yi[k * M + m], v) + v); });
+          mm.template run2<true, false, false, true, WIMG>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
+                                                     [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&yi[k * M + m], v) + v); },
+                                                     a.img_abT[l]);
         } else {
           // bottom layer: the embedding's output tanh derivative (dp_core.hpp:580-583) is
           // applied in the same epilogue, dX0 (1 - X0^2)
           const float* x0 = X;
-          mm.template run2<true, false, false, true>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
+          mm.template run2<true, false, false, true, WIMG>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
                                                      [=](int k, int m, auto v) {
                                                        vst(&xo[k * M + m], (vld(&yi[k * M + m], v) + v) * vdtanh(vld(&x0[k * M + m], v)));
-                                                     });
+                                                     },
+                                                     a.img_abT[l]);
         }
       }
       __syncthreads();
@@ -721,10 +728,11 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       for (int e = a.n_embed - 1; e >= 1; --e) {
         const int Ein = a.edims[e - 1], Eout = a.edims[e];
         const float* h = a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride + offs[e - 1];
-        mm.template run<false, false>(n, Ein, Eout, dY, Eout, a.ew[e], Ein,
-                            [&](int k, int i, auto v) {
-                              vst(&dXn[k * Ein + i], v * vdtanh(vld(&h[k * Ein + i], v)));
-                            });
+        mm.template run<false, false, 0, 1, WIMG>(n, Ein, Eout, dY, Eout, a.ew[e], Ein,
+                                                  [&](int k, int i, auto v) {
+                                                    vst(&dXn[k * Ein + i], v * vdtanh(vld(&h[k * Ein + i], v)));
+                                                  },
+                                                  a.img_ewT[e]);
         __syncthreads();
         float* tmp = dY;
         dY = dXn;
@@ -824,6 +832,41 @@ __global__ void __launch_bounds__(256) k_env(const __grid_constant__ DpArgs a) {
   if (lane == 0) a.sig[c] = sig;
 }
 
+// Pre-split weight image of a GEMM's B operand (tc::bulk_g2s): B(k, n) = TB ? W[n*ldb + k]
+// : W[k*ldb + n], K x N, per 32-wide K chunk [hi | lo] of NT rows x 128 bytes, K-major
+// SW128.  Built once per context; the per-centre GEMMs then stage it with two bulk copies.
+__global__ void k_weight_image(const float* __restrict__ W, int TB, int ldb, int K, int N, int NT,
+                               uint8_t* __restrict__ out) {
+  const int nch = (K + tc::kKC - 1) / tc::kKC;
+  const long total = static_cast<long>(nch) * NT * tc::kKC;
+  for (long e = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int kl = static_cast<int>(e % tc::kKC);
+    const int n = static_cast<int>((e / tc::kKC) % NT);
+    const int c = static_cast<int>(e / (static_cast<long>(tc::kKC) * NT));
+    const int k = c * tc::kKC + kl;
+    float v = 0.f;
+    if (n < N && k < K) v = TB ? W[static_cast<size_t>(n) * ldb + k] : W[static_cast<size_t>(k) * ldb + n];
+    const float hi = tc::tf32_rn(v);
+    uint8_t* img = out + static_cast<size_t>(c) * 2 * NT * 128;
+    const uint32_t off = tc::sw128_off(n, kl);
+    *reinterpret_cast<float*>(img + off) = hi;
+    *reinterpret_cast<float*>(img + static_cast<size_t>(NT) * 128 + off) = v - hi;
+  }
+}
+
+size_t weight_image_bytes(int K, int N) {
+  const int nch = (K + tc::kKC - 1) / tc::kKC;
+  const int NT = (N + 15) & ~15;
+  return static_cast<size_t>(nch) * 2 * NT * 128;
+}
+
+void launch_weight_image(const float* W, int TB, int ldb, int K, int N, uint8_t* out, cudaStream_t st) {
+  const int NT = (N + 15) & ~15;
+  k_weight_image<<<128, 256, 0, st>>>(W, TB, ldb, K, N, NT, out);
+  count_launch();
+}
+
 void launch_env(const DpArgs& a, cudaStream_t st) {
   if (a.n_centres == 0) return;
   const long threads = static_cast<long>(a.n_centres) * 32;
@@ -831,37 +874,40 @@ void launch_env(const DpArgs& a, cudaStream_t st) {
   count_launch();
 }
 
-template <int MODE>
+template <int MODE, bool WIMG>
 static void set_smem(size_t smem) {
   static size_t done = 0;
   if (smem > done) {
-    cudaFuncSetAttribute(k_centre_forward<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_centre_backward<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_centre_forward<MODE, WIMG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_centre_backward<MODE, WIMG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     done = smem;
   }
 }
 
-void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st) {
+// a.wimg: every weight GEMM has a pre-split image (tensor-core modes) -> the WIMG kernels
+template <bool FWD>
+static void launch_centre(const DpArgs& a, int grid, cudaStream_t st) {
   if (a.n_centres == 0) return;
   const size_t smem = dp_smem_bytes(a, a.mode);
-  switch (a.mode) {
-    case 0: set_smem<0>(smem); k_centre_forward<0><<<grid, 256, smem, st>>>(a); break;
-    case 1: set_smem<1>(smem); k_centre_forward<1><<<grid, 256, smem, st>>>(a); break;
-    default: set_smem<2>(smem); k_centre_forward<2><<<grid, 256, smem, st>>>(a); break;
-  }
+  auto go = [&](auto mode_c, auto wimg_c) {
+    constexpr int MODE = decltype(mode_c)::value;
+    constexpr bool WIMG = decltype(wimg_c)::value;
+    set_smem<MODE, WIMG>(smem);
+    if (FWD) k_centre_forward<MODE, WIMG><<<grid, 256, smem, st>>>(a);
+    else k_centre_backward<MODE, WIMG><<<grid, 256, smem, st>>>(a);
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  if (a.mode == 0) go(std::integral_constant<int, 0>{}, F{});
+  else if (a.mode == 1 && a.wimg) go(std::integral_constant<int, 1>{}, T{});
+  else if (a.mode == 1) go(std::integral_constant<int, 1>{}, F{});
+  else if (a.wimg) go(std::integral_constant<int, 2>{}, T{});
+  else go(std::integral_constant<int, 2>{}, F{});
   count_launch();
 }
 
-void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st) {
-  if (a.n_centres == 0) return;
-  const size_t smem = dp_smem_bytes(a, a.mode);
-  switch (a.mode) {
-    case 0: set_smem<0>(smem); k_centre_backward<0><<<grid, 256, smem, st>>>(a); break;
-    case 1: set_smem<1>(smem); k_centre_backward<1><<<grid, 256, smem, st>>>(a); break;
-    default: set_smem<2>(smem); k_centre_backward<2><<<grid, 256, smem, st>>>(a); break;
-  }
-  count_launch();
-}
+void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st) { launch_centre<true>(a, grid, st); }
+void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st) { launch_centre<false>(a, grid, st); }
 
 // ------------------------------------------------------------------------------------
 // Fitting net over all centres (dp_core.hpp:386-391 forward; 408-414 backward)

@@ -164,7 +164,18 @@ struct DpArgs {
   int mode;             // 0 SIMT FP32, 1 3xTF32 tcgen05, 2 1xTF32 tcgen05
   unsigned long long* prof;  // optional per-phase cycle counters (thread 0 of each CTA)
   int flags;            // experiment switches (NNMD_FLAGS): bit0 no L2 prefetch, bit1 unfused row pass
+  // pre-split weight images (launch_weight_image) of the per-centre weight GEMMs' B
+  // operands, or NULL: U = X [A|B], dX += dU [A|B]^T, embedding forward / backward
+  const uint8_t* img_ab[16];
+  const uint8_t* img_abT[16];
+  const uint8_t* img_ew[kMaxLayers];
+  const uint8_t* img_ewT[kMaxLayers];
+  int wimg;  // 1: all of the above are present (the per-centre kernels' WIMG variant)
 };
+// Weight images: bytes for a K x N operand, and the builder (B(k,n) = TB ? W[n*ldb+k] :
+// W[k*ldb+n]).
+size_t weight_image_bytes(int K, int N);
+void launch_weight_image(const float* W, int TB, int ldb, int K, int N, uint8_t* out, cudaStream_t st);
 size_t dp_scratch_floats(const DpArgs& a);
 size_t dp_smem_bytes(const DpArgs& a, int mode);
 // Environment matrix: FP64 geometry (image_delta, r, switch) -> float4 env rows, species,

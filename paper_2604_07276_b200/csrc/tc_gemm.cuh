@@ -38,6 +38,7 @@ struct alignas(1024) Smem {
   uint8_t a[NST][2][kMT * 128];  // [stage][hi/lo]  16 KB each
   uint8_t b[NST][2][kNT * 128];  // [stage][hi/lo]  32 KB each
   uint64_t bar[2];
+  uint64_t tbar;  // bulk-copy (TMA) completion of pre-split weight images
   uint32_t tmem_base;
   uint32_t pad;
 };
@@ -51,6 +52,8 @@ struct State {
   int nst;
   int cols;             // allocated TMEM columns (256, or 512 with promotion)
   uint32_t tmem;
+  uint64_t* tbar;       // weight-image bulk copies
+  uint32_t tph;         // bulk-copy phases consumed (thread 0)
   uint32_t uses[2];     // commits issued per stage
   uint32_t waited[2];   // commits waited per stage
   unsigned long long* prof;  // optional: thread 0 accumulates cycles per GEMM stage (ids 0..7)
@@ -122,6 +125,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Pre-split weight images (built once per context, model.cpp / k_weight_image): the B
+// operand of a weight GEMM as it sits in the shared-memory stage, per 32-wide K chunk
+// [hi | lo] of NT rows x 128 bytes, K-major SW128 (swizzle relative to a 1024-aligned
+// base).  One thread moves a chunk with two 1-D bulk copies (TMA engine); no register or
+// st.shared traffic for that operand.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() {
@@ -167,6 +186,8 @@ __device__ __forceinline__ void init(State& st, Smem<NST>* sm, int cols) {
       st.b[s][p] = sm->b[s % NST][p];
     }
   st.bar = sm->bar;
+  st.tbar = &sm->tbar;
+  st.tph = 0;
   st.tmem_slot = &sm->tmem_base;
   st.nst = NST;
   st.cols = cols;
@@ -185,6 +206,7 @@ __device__ __forceinline__ void init(State& st, Smem<NST>* sm, int cols) {
   if (threadIdx.x == 32) {
     mbar_init(&sm->bar[0], 1);
     mbar_init(&sm->bar[1], 1);
+    mbar_init(&sm->tbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   fence_before();
@@ -311,10 +333,14 @@ __device__ __forceinline__ void store_chunk(int R, const Frag<MAXV>& f, uint8_t*
 // with float4 for 4 consecutive aligned columns); 2 tile functor, called once per column
 // block by all threads with the SMEM-staged accumulator tile:
 // epi(const float* stg, int ldst, int mrows, int ncols, int m_base, int n_base).
-template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int PROMOTE, int NST, int EK = 1, class Epi>
+// IMG1 / IMG2: B / B2 come from pre-split weight images img1 / img2 (N <= kNT; see
+// bulk_g2s) instead of being loaded and split by the threads.
+template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int PROMOTE, int NST, int EK = 1, bool IMG1 = false,
+          bool IMG2 = false, class Epi>
 __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
                                       const float* __restrict__ B, int ldb, int K2, const float* __restrict__ A2,
-                                      int lda2, const float* __restrict__ B2, int ldb2, Epi epi) {
+                                      int lda2, const float* __restrict__ B2, int ldb2, Epi epi,
+                                      const uint8_t* img1 = nullptr, const uint8_t* img2 = nullptr) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   constexpr bool two = NPASS > 1;
@@ -328,13 +354,18 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
       // A: 128 rows -> 4 float4 per thread either way; B: NT <= 256 rows -> <= 8
       Frag<4> fa;
       Frag<8> fb;
+      const uint32_t img_bytes = static_cast<uint32_t>(NT) * 128u;  // one of hi / lo
+      auto img_of = [&](int c) -> const uint8_t* {
+        if (c < nch1) return IMG1 ? img1 + static_cast<size_t>(c) * 2 * img_bytes : nullptr;
+        return IMG2 ? img2 + static_cast<size_t>(c - nch1) * 2 * img_bytes : nullptr;
+      };
       auto load = [&](int c) {
         if (c < nch1) {
           load_chunk<TA, 4>(A, lda, M, K, m0, c * kKC, kMT, fa);
-          load_chunk<!TB, 8>(B, ldb, N, K, n0, c * kKC, NT, fb);
+          if (!IMG1) load_chunk<!TB, 8>(B, ldb, N, K, n0, c * kKC, NT, fb);
         } else {
           load_chunk<TA2, 4>(A2, lda2, M, K2, m0, (c - nch1) * kKC, kMT, fa);
-          load_chunk<!TB2, 8>(B2, ldb2, N, K2, n0, (c - nch1) * kKC, NT, fb);
+          if (!IMG2) load_chunk<!TB2, 8>(B2, ldb2, N, K2, n0, (c - nch1) * kKC, NT, fb);
         }
       };
       st.tick(-1);
@@ -348,18 +379,29 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
         uint8_t* al = st.a[s][1];
         uint8_t* bh = st.b[s][0];
         uint8_t* bl = st.b[s][1];
+        const uint8_t* img = (IMG1 || IMG2) ? img_of(c) : nullptr;
+        if ((IMG1 || IMG2) && img && tid == 0) {
+          // weight operand: two bulk copies, overlapping the A staging below
+          mbar_expect_tx(st.tbar, 2 * img_bytes);
+          bulk_g2s(bh, img, img_bytes, st.tbar);
+          bulk_g2s(bl, img + img_bytes, img_bytes, st.tbar);
+        }
         if (c < nch1) {
           store_chunk<TA, 4>(kMT, fa, ah, al, two);
-          store_chunk<!TB, 8>(NT, fb, bh, bl, two);
+          if (!IMG1) store_chunk<!TB, 8>(NT, fb, bh, bl, two);
         } else {
           store_chunk<TA2, 4>(kMT, fa, ah, al, two);
-          store_chunk<!TB2, 8>(NT, fb, bh, bl, two);
+          if (!IMG2) store_chunk<!TB2, 8>(NT, fb, bh, bl, two);
         }
         st.tick(2);
         fence_proxy_async();
         __syncthreads();
         st.tick(3);
         if (tid == 0) {
+          if ((IMG1 || IMG2) && img) {
+            mbar_wait(st.tbar, st.tph & 1u);
+            ++st.tph;
+          }
           fence_after();
           const uint32_t a0 = smem_u32(ah), a1 = smem_u32(al), b0 = smem_u32(bh), b1 = smem_u32(bl);
 #pragma unroll
@@ -528,10 +570,12 @@ __device__ __forceinline__ void load_arow(const float* __restrict__ A, int lda, 
   }
 }
 
-template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int EK = 1, class Epi>
+template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int EK = 1, bool IMG1 = false, bool IMG2 = false,
+          class Epi>
 __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
                                          const float* __restrict__ B, int ldb, int K2, const float* __restrict__ A2,
-                                         int lda2, const float* __restrict__ B2, int ldb2, Epi epi) {
+                                         int lda2, const float* __restrict__ B2, int ldb2, Epi epi,
+                                         const uint8_t* img1 = nullptr, const uint8_t* img2 = nullptr) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   constexpr bool two = NPASS > 1;
@@ -548,13 +592,18 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
       const uint32_t idesc = idesc_tf32(NT);
       float av[16];
       Frag<4> fb;
+      const uint32_t img_bytes = static_cast<uint32_t>(NT) * 128u;
+      auto img_of = [&](int c) -> const uint8_t* {
+        if (c < nch1) return IMG1 ? img1 + static_cast<size_t>(c) * 2 * img_bytes : nullptr;
+        return IMG2 ? img2 + static_cast<size_t>(c - nch1) * 2 * img_bytes : nullptr;
+      };
       auto load = [&](int c) {
         if (c < nch1) {
           load_arow<TA>(A, lda, M, K, m0 + arow, c * kKC + akof, av);
-          load_chunk<!TB, 4>(B, ldb, N, K, n0, c * kKC, NT, fb);
+          if (!IMG1) load_chunk<!TB, 4>(B, ldb, N, K, n0, c * kKC, NT, fb);
         } else {
           load_arow<TA2>(A2, lda2, M, K2, m0 + arow, (c - nch1) * kKC + akof, av);
-          load_chunk<!TB2, 4>(B2, ldb2, N, K2, n0, (c - nch1) * kKC, NT, fb);
+          if (!IMG2) load_chunk<!TB2, 4>(B2, ldb2, N, K2, n0, (c - nch1) * kKC, NT, fb);
         }
       };
       st.tick(-1);
@@ -577,8 +626,18 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
         }
         uint8_t* bh = base + 32768 * s;
         uint8_t* bl = bh + 16384;
-        if (c < nch1) store_chunk<!TB, 4>(NT, fb, bh, bl, two);
-        else store_chunk<!TB2, 4>(NT, fb, bh, bl, two);
+        const uint8_t* img = (IMG1 || IMG2) ? img_of(c) : nullptr;
+        if ((IMG1 || IMG2) && img) {
+          if (tid == 0) {
+            mbar_expect_tx(st.tbar, 2 * img_bytes);
+            bulk_g2s(bh, img, img_bytes, st.tbar);
+            bulk_g2s(bl, img + img_bytes, img_bytes, st.tbar);
+          }
+        } else if (c < nch1) {
+          store_chunk<!TB, 4>(NT, fb, bh, bl, two);
+        } else {
+          store_chunk<!TB2, 4>(NT, fb, bh, bl, two);
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         st.tick(2);
         fence_before();
@@ -586,6 +645,10 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
         __syncthreads();
         st.tick(3);
         if (tid == 0) {
+          if ((IMG1 || IMG2) && img) {
+            mbar_wait(st.tbar, st.tph & 1u);
+            ++st.tph;
+          }
           fence_after();
           const uint32_t ah = st.tmem + kTsA + 64u * s, al = ah + 32;
           const uint32_t b0 = smem_u32(bh), b1 = smem_u32(bl);
@@ -665,16 +728,16 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
   }
 }
 
-template <bool TA, bool TB, int NPASS, int EK = 1, class Epi>
+template <bool TA, bool TB, int NPASS, int EK = 1, bool IMG = false, class Epi>
 __device__ __forceinline__ void gemm_ts(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
-                                        const float* __restrict__ B, int ldb, Epi epi) {
-  gemm2_ts<TA, TB, TA, TB, NPASS, EK>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi);
+                                        const float* __restrict__ B, int ldb, Epi epi, const uint8_t* img = nullptr) {
+  gemm2_ts<TA, TB, TA, TB, NPASS, EK, IMG, false>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi, img);
 }
 
-template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, int EK = 1, class Epi>
+template <bool TA, bool TB, int NPASS, int PROMOTE = 0, int NST = 2, int EK = 1, bool IMG = false, class Epi>
 __device__ __forceinline__ void gemm(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
-                                     const float* __restrict__ B, int ldb, Epi epi) {
-  gemm2<TA, TB, TA, TB, NPASS, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi);
+                                     const float* __restrict__ B, int ldb, Epi epi, const uint8_t* img = nullptr) {
+  gemm2<TA, TB, TA, TB, NPASS, PROMOTE, NST, EK, IMG, false>(st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi, img);
 }
 
 }  // namespace tc
