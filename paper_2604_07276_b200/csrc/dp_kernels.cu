@@ -234,45 +234,67 @@ __device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, c
   }
 }
 
+// Register-cached rows (n <= 32 C): each lane keeps its C key columns' s_j^2 and R_j for
+// all of its warp's rows.
+template <int C>
+__device__ void softmax_gate_rc(int n, int ln, const float* S, int lds, float* PU, float* PT, float inv_sig,
+                                const Smem& sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float s2[C];
+  float4 Rj[C];
+#pragma unroll
+  for (int t = 0; t < C; ++t) {
+    const int j = lane + 32 * t;
+    s2[t] = j < n ? sm.s[j] * sm.s[j] : 0.f;
+    Rj[t] = j < n ? sm.R[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int k = wid; k < n; k += nw) {
+    const float* row = S + static_cast<size_t>(k) * lds;
+    float e[C];
+    float mx = -FLT_MAX;
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      const int j = lane + 32 * t;
+      e[t] = j < n ? row[j] : -FLT_MAX;
+      mx = fmaxf(mx, e[t]);
+    }
+    mx = warp_max(mx);
+    float den = 0.f;
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      const int j = lane + 32 * t;
+      e[t] = j < n ? __expf(e[t] - mx) : 0.f;
+      den += s2[t] * e[t];
+    }
+    den = warp_sum(den);
+    const float inv = den > 0.f ? 1.0f / den : 0.f;
+    const float4 Rk = sm.R[k];
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      const int j = lane + 32 * t;
+      if (j < n) {
+        const float pu = e[t] * inv;
+        if (PU) PU[static_cast<size_t>(k) * ln + j] = pu;
+        PT[static_cast<size_t>(k) * ln + j] = s2[t] * pu * (dot4(Rk, Rj[t]) * inv_sig);
+      }
+    }
+  }
+}
+
 // Weighted softmax + gate for every row: PU = pu (optional), PT = s_j^2 pu Theta.
 __device__ void softmax_gate(int n, int ln, const float* S, int lds, float* PU, float* PT, float inv_sig,
                              const Smem& sm) {
+  if (n <= 128) {
+    softmax_gate_rc<4>(n, ln, S, lds, PU, PT, inv_sig, sm);
+    return;
+  }
+  if (n <= 256) {
+    softmax_gate_rc<8>(n, ln, S, lds, PU, PT, inv_sig, sm);
+    return;
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  constexpr int kMaxC = 8;  // register-cached row chunks: n <= 256
   for (int k = wid; k < n; k += nw) {
     const float* row = S + static_cast<size_t>(k) * lds;
-    if (n <= 32 * kMaxC) {
-      float e[kMaxC];
-      float mx = -FLT_MAX;
-#pragma unroll
-      for (int t = 0; t < kMaxC; ++t) {
-        const int j = lane + 32 * t;
-        e[t] = j < n ? row[j] : -FLT_MAX;
-        mx = fmaxf(mx, e[t]);
-      }
-      mx = warp_max(mx);
-      float den = 0.f;
-#pragma unroll
-      for (int t = 0; t < kMaxC; ++t) {
-        const int j = lane + 32 * t;
-        e[t] = j < n ? expf(e[t] - mx) : 0.f;
-        if (j < n) den += sm.s[j] * sm.s[j] * e[t];
-      }
-      den = warp_sum(den);
-      const float inv = den > 0.f ? 1.0f / den : 0.f;
-      const float4 Rk = sm.R[k];
-#pragma unroll
-      for (int t = 0; t < kMaxC; ++t) {
-        const int j = lane + 32 * t;
-        if (j < n) {
-          const float sj = sm.s[j];
-          const float pu = e[t] * inv;
-          if (PU) PU[static_cast<size_t>(k) * ln + j] = pu;
-          PT[static_cast<size_t>(k) * ln + j] = sj * sj * pu * (dot4(Rk, sm.R[j]) * inv_sig);
-        }
-      }
-      continue;
-    }
     float mx = -FLT_MAX;
     for (int j = lane; j < n; j += 32) mx = fmaxf(mx, row[j]);
     mx = warp_max(mx);
