@@ -355,12 +355,27 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   cell_start_.ensure(ncell + 1);
   cell_fill_.ensure(ncell + 1);
   cell_members_.ensure(nm + 1);
+  cs_x_.ensure(3 * static_cast<size_t>(nm) + 3);
+  cs_i_.ensure(2 * static_cast<size_t>(nm) + 2);
+  cs_gid_.ensure(static_cast<size_t>(nm) + 1);
+  CellSorted csd{};
+  csd.pos = sys.pos;
+  csd.atom_species = sys.species;
+  csd.atom_gid = sys.gid;
+  csd.m_atom = m_atom_.p;
+  csd.m_shift = m_shift_.p;
+  csd.x = cs_x_.p;
+  csd.y = cs_x_.p + nm;
+  csd.z = cs_x_.p + 2 * static_cast<size_t>(nm);
+  csd.shift = cs_i_.p;
+  csd.species = cs_i_.p + nm;
+  csd.gid = cs_gid_.p;
   tic("cells");
   CU(cudaMemsetAsync(cell_count_.p, 0, (ncell + 1) * sizeof(int), st_));
   CU(cudaMemsetAsync(cell_fill_.p, 0, (ncell + 1) * sizeof(int), st_));
   launch_cell_count(cg, m_pos_.p, nm, m_cell_.p, cell_count_.p, st_);
   launch_scan(cell_count_.p, cell_start_.p, static_cast<int>(ncell), st_);
-  launch_cell_fill(m_cell_.p, nm, cell_start_.p, cell_fill_.p, cell_members_.p, st_);
+  launch_cell_fill(m_cell_.p, nm, cell_start_.p, cell_fill_.p, cell_members_.p, csd, st_);
   toc();
   const int nmax = m.n_max;
   nlist_.ensure(static_cast<size_t>(ncen) * nmax + 1);
@@ -378,6 +393,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   na.m_cell = m_cell_.p;
   na.cell_start = cell_start_.p;
   na.cell_members = cell_members_.p;
+  na.cs = csd;
   na.n_max = nmax;
   na.rc2 = m.rc * m.rc;
   na.centre_member = cen_member_.p;

@@ -141,6 +141,9 @@ class Context {
   DevBuf<int> m_atom_, m_shift_, m_owner_, m_cell_, cflag_, coff_, cen_member_, cidx_;
   DevBuf<double> m_pos_;
   DevBuf<int> cell_count_, cell_start_, cell_fill_, cell_members_;
+  DevBuf<double> cs_x_;      // cell-ordered candidate positions (x | y | z)
+  DevBuf<int> cs_i_;         // cell-ordered packed shift | species
+  DevBuf<int64_t> cs_gid_;   // cell-ordered gids
   DevBuf<int> nlist_, nn_, rlist_, rn_;
   DevBuf<float> X_, Ad_, Bd_, D_, dD_, scratch_, fitY_, fitd_, Ust_, PUst_, PTst_, EMBst_;
   DevBuf<float4> R_;

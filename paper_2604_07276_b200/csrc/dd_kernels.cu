@@ -234,19 +234,31 @@ void launch_cell_count(const CellArgs& c, const double* m_pos, int n, int* m_cel
   k_cell_count<<<(n + 255) / 256, 256, 0, st>>>(c, m_pos, n, m_cell, count); count_launch();
 }
 
+// Fill the cell lists and a cell-ordered copy of what the neighbour scan reads per
+// candidate (atom position, packed shift, species, gid), so that scan's loads are
+// contiguous across a warp instead of chasing member -> atom indirections.  The order
+// inside a cell is arbitrary: rows are sorted by the canonical key afterwards.
 __global__ void k_cell_fill(const int* __restrict__ m_cell, int n, const int* __restrict__ start,
-                            int* __restrict__ fill, int* __restrict__ members) {
+                            int* __restrict__ fill, int* __restrict__ members, CellSorted cs) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
   const int id = m_cell[m];
   const int slot = atomicAdd(&fill[id], 1);
-  members[start[id] + slot] = m;
+  const int j = start[id] + slot;
+  members[j] = m;
+  const int aj = cs.m_atom[m];
+  cs.x[j] = cs.pos[3 * aj];
+  cs.y[j] = cs.pos[3 * aj + 1];
+  cs.z[j] = cs.pos[3 * aj + 2];
+  cs.shift[j] = cs.m_shift[m];
+  cs.species[j] = cs.atom_species[aj];
+  cs.gid[j] = cs.atom_gid[aj];
 }
 
-void launch_cell_fill(const int* m_cell, int n, const int* start, int* fill, int* members,
+void launch_cell_fill(const int* m_cell, int n, const int* start, int* fill, int* members, const CellSorted& cs,
                       cudaStream_t st) {
   if (n == 0) return;
-  k_cell_fill<<<(n + 255) / 256, 256, 0, st>>>(m_cell, n, start, fill, members); count_launch();
+  k_cell_fill<<<(n + 255) / 256, 256, 0, st>>>(m_cell, n, start, fill, members, cs); count_launch();
 }
 
 // ----------------------------------------------------------------------------------
@@ -304,19 +316,18 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
           if (j < e) {
             const int mj = a.cell_members[j];
             if (mj != cm && mj < a.cand_limit) {
-              const int aj = a.m_atom[mj];
-              const int sj = a.m_shift[mj];
+              const int sj = a.cs.shift[j];
               const int rel[3] = {shift_x(sj) - csh[0], shift_y(sj) - csh[1], shift_z(sj) - csh[2]};
-              const double dx = image_delta(a.pos[3 * aj], pc[0], rel[0], a.L[0]);
-              const double dy = image_delta(a.pos[3 * aj + 1], pc[1], rel[1], a.L[1]);
-              const double dz = image_delta(a.pos[3 * aj + 2], pc[2], rel[2], a.L[2]);
+              const double dx = image_delta(a.cs.x[j], pc[0], rel[0], a.L[0]);
+              const double dy = image_delta(a.cs.y[j], pc[1], rel[1], a.L[1]);
+              const double dz = image_delta(a.cs.z[j], pc[2], rel[2], a.L[2]);
               const double r2 = norm2_exact(dx, dy, dz);
               if (r2 < a.rc2) {
                 keep = true;
                 ent.r2 = r2;
-                ent.gid = a.gid[aj];
+                ent.gid = a.cs.gid[j];
                 ent.member = mj;
-                ent.species = a.species[aj];
+                ent.species = a.cs.species[j];
               }
             }
           }
@@ -379,7 +390,6 @@ __global__ void __launch_bounds__(128) k_force_gather(ForceArgs a) {
     const double* g = a.g + static_cast<size_t>(oc) * a.n_max * 3;
     for (int k = lane; k < n; k += 32)
       for (int c = 0; c < 3; ++c) own[c] += g[3 * k + c];
-    for (int c = 0; c < 3; ++c) own[c] = warp_sum(own[c]);
   }
   const int* list;
   int cnt;
@@ -390,25 +400,37 @@ __global__ void __launch_bounds__(128) k_force_gather(ForceArgs a) {
     list = a.rlist + static_cast<size_t>(t - a.nloc) * a.n_max;
     cnt = a.rn[t - a.nloc];
   }
+  // lane per incoming centre c: find t's row k in c's list (16-byte loads), take g[c][k]
   double in[3] = {0, 0, 0};
-  for (int e = 0; e < cnt; ++e) {
+  for (int e = lane; e < cnt; e += 32) {
     const int c = a.cidx[list[e]];
     if (c < 0) continue;
     const int nc = a.nn[c];
     const int* row = a.nlist + static_cast<size_t>(c) * a.n_max;
     int k = -1;
-    for (int base = 0; base < nc && k < 0; base += 32) {
-      const int j = base + lane;
-      const unsigned hit = __ballot_sync(0xffffffffu, j < nc && row[j] == t);
-      if (hit) k = base + __ffs(hit) - 1;
+    const bool vec = (a.n_max & 3) == 0;
+    if (vec) {
+      for (int b = 0; b < nc && k < 0; b += 4) {
+        const int4 q = *reinterpret_cast<const int4*>(row + b);
+        if (q.x == t) k = b;
+        else if (q.y == t && b + 1 < nc) k = b + 1;
+        else if (q.z == t && b + 2 < nc) k = b + 2;
+        else if (q.w == t && b + 3 < nc) k = b + 3;
+      }
+      if (k >= nc) k = -1;
+    } else {
+      for (int b = 0; b < nc && k < 0; ++b)
+        if (row[b] == t) k = b;
     }
     if (k >= 0) {
       const double* g = a.g + (static_cast<size_t>(c) * a.n_max + k) * 3;
       for (int q = 0; q < 3; ++q) in[q] += g[q];
     }
   }
-  if (lane == 0)
-    for (int q = 0; q < 3; ++q) a.fmem[3 * static_cast<size_t>(t) + q] = own[q] - in[q];
+  for (int q = 0; q < 3; ++q) {
+    const double v = warp_sum(own[q]) - warp_sum(in[q]);
+    if (lane == 0) a.fmem[3 * static_cast<size_t>(t) + q] = v;
+  }
 }
 
 void launch_force_gather(const ForceArgs& a, cudaStream_t st) {

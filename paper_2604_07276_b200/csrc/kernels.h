@@ -53,8 +53,20 @@ struct CellArgs {
 };
 void launch_cell_count(const CellArgs& c, const double* m_pos, int n_members, int* m_cell,
                        int* cell_count, cudaStream_t st);
+// cell-ordered copies of the per-candidate inputs of the neighbour scan (k_cell_fill)
+struct CellSorted {
+  const double* pos;          // atom positions [n][3]
+  const int* atom_species;
+  const int64_t* atom_gid;
+  const int* m_atom;
+  const int* m_shift;
+  double *x, *y, *z;          // [members], cell order
+  int* shift;
+  int* species;
+  int64_t* gid;
+};
 void launch_cell_fill(const int* m_cell, int n_members, const int* cell_start, int* cell_fill,
-                      int* cell_members, cudaStream_t st);
+                      int* cell_members, const CellSorted& cs, cudaStream_t st);
 
 struct NbrArgs {
   const double* pos;
@@ -66,6 +78,7 @@ struct NbrArgs {
   const int* m_cell;
   const int* cell_start;
   const int* cell_members;
+  CellSorted cs;             // cell-ordered candidate data (same index as cell_members)
   int cdims[3];
   const int* centre_member;  // member index of each list owner (NULL: li + member_offset)
   int member_offset;
