@@ -426,6 +426,7 @@ __device__ void bwd_col_pass(int n, int ln, int stride, const float* TS, int ldt
     r.w += p0.w + p1.w;
     sm.dR[j] = r;
   }
+  tc::fence_proxy_async();  // part may sit in an operand stage that bulk copies overwrite later
 }
 
 }  // namespace
@@ -593,6 +594,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         for (int i = threadIdx.x; i < M * mr; i += blockDim.x) tmp[i] = dD[i];
         for (int i = threadIdx.x; i < M * 4; i += blockDim.x) tmp[M * mr + i] = Ad[i];
         for (int i = threadIdx.x; i < 4 * mr; i += blockDim.x) tmp[M * mr + M * 4 + i] = Bd[i];
+        tc::fence_proxy_async();  // operand-stage memory: later overwritten by bulk copies
         __syncthreads();
         sdD = tmp;
         sAd = tmp + M * mr;
