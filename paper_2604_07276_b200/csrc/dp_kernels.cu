@@ -509,20 +509,45 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
       pc.mark(5);
     }
     // descriptor (dp_core.hpp:358-384)
+    // A = X^T R: thread per (feature m, k-half), all four R components at once, coalesced
+    // over m; the two k-halves are added in a fixed order.  B = R^T X_< is the same sums
+    // (B[q][r] = A[r][q] before scaling, product for product), so it is copied.
     const float* Xf = X + a.n_attn * a.x_layer_stride;
-    for (int idx = threadIdx.x; idx < M * 4 + 4 * mr; idx += blockDim.x) {
-      float acc = 0.f;
-      if (idx < M * 4) {
-        const int m = idx >> 2, q = idx & 3;
-        for (int k = 0; k < n; ++k) acc += Xf[k * M + m] * reinterpret_cast<const float*>(&sm.R[k])[q];
-        sm.Ad[idx] = acc * a.inv_sqrt_nmax;
-      } else {
-        const int j = idx - M * 4, q = j / mr, r = j - q * mr;
-        for (int k = 0; k < n; ++k) acc += reinterpret_cast<const float*>(&sm.R[k])[q] * Xf[k * M + r];
-        sm.Bd[j] = acc * a.inv_sqrt_nmax;
+    {
+      float4* part = reinterpret_cast<float4*>(sm.head);  // [2][M]; operand stages idle
+      const int nh = (n + 1) >> 1;
+      const int half_threads = blockDim.x >> 1;
+      const int h = threadIdx.x / half_threads;
+      const int kb = h * nh, ke = min(n, kb + nh);
+      for (int m = threadIdx.x - h * half_threads; m < M; m += half_threads) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+        for (int k = kb; k < ke; ++k) {
+          const float x = Xf[k * M + m];
+          const float4 R = sm.R[k];
+          a0 += x * R.x;
+          a1 += x * R.y;
+          a2 += x * R.z;
+          a3 += x * R.w;
+        }
+        part[h * M + m] = make_float4(a0, a1, a2, a3);
       }
+      tc::fence_proxy_async();  // operand-stage memory: later overwritten by bulk copies
+      __syncthreads();
+      for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        const float4 p0 = part[m], p1 = part[M + m];
+        const float4 A = make_float4((p0.x + p1.x) * a.inv_sqrt_nmax, (p0.y + p1.y) * a.inv_sqrt_nmax,
+                                     (p0.z + p1.z) * a.inv_sqrt_nmax, (p0.w + p1.w) * a.inv_sqrt_nmax);
+        reinterpret_cast<float4*>(sm.Ad)[m] = A;
+        if (m < mr) {
+          sm.Bd[0 * mr + m] = A.x;
+          sm.Bd[1 * mr + m] = A.y;
+          sm.Bd[2 * mr + m] = A.z;
+          sm.Bd[3 * mr + m] = A.w;
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
     float* D = a.D + static_cast<size_t>(c) * M * mr;
     for (int idx = threadIdx.x; idx < M * mr; idx += blockDim.x) {
       const int m = idx / mr, q = idx - m * mr;
@@ -591,7 +616,12 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       const float* sBd = Bd;
       if constexpr (MODE != 0) {
         float* tmp = reinterpret_cast<float*>(sm.head);
-        for (int i = threadIdx.x; i < M * mr; i += blockDim.x) tmp[i] = dD[i];
+        if (((M * mr) & 3) == 0) {
+          for (int i = threadIdx.x; i < (M * mr) >> 2; i += blockDim.x)
+            reinterpret_cast<float4*>(tmp)[i] = reinterpret_cast<const float4*>(dD)[i];
+        } else {
+          for (int i = threadIdx.x; i < M * mr; i += blockDim.x) tmp[i] = dD[i];
+        }
         for (int i = threadIdx.x; i < M * 4; i += blockDim.x) tmp[M * mr + i] = Ad[i];
         for (int i = threadIdx.x; i < 4 * mr; i += blockDim.x) tmp[M * mr + M * 4 + i] = Bd[i];
         tc::fence_proxy_async();  // operand-stage memory: later overwritten by bulk copies
