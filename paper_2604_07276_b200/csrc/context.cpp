@@ -403,6 +403,9 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   na.nn = nn_.p;
   na.err = err_.p + 1;
   na.nonempty = nullptr;
+  maxn_.ensure(1);
+  CU(cudaMemsetAsync(maxn_.p, 0, sizeof(int), st_));
+  na.maxn = maxn_.p;
   tic("neighbors");
   launch_neighbors(na, st_);
   toc();
@@ -414,6 +417,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     rv.member_offset = nloc;
     rv.n_lists = ngh;
     rv.cand_limit = nloc;
+    rv.maxn = nullptr;
     rv.nlist = rlist_.p;
     rv.nn = rn_.p;
     rv.err = err_.p + 2;
@@ -516,6 +520,15 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     }
     dp.wimg = all ? 1 : 0;
   }
+  // on-chip chained forward (experimental, opt-in with NNMD_FWD2=1): needs
+  // the weight images, M = 128 and every centre's n <= 128 (one host read-back of the
+  // largest row count).  Measured slower than the two-CTA forward (14.6 vs 9.2 ms).
+  static const bool fwd2_on = getenv("NNMD_FWD2") && getenv("NNMD_FWD2")[0] == '1';
+  if (fwd2_on && dp.wimg && M == 128 && m.na >= 1 && opts_.precision != NNMD_PREC_FP32_SIMT) {
+    CU(cudaMemcpyAsync(h_counts_ + 12, maxn_.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    CU(cudaStreamSynchronize(st_));
+    dp.fwd2 = h_counts_[12] <= 128 ? 1 : 0;
+  }
   dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
   const int grid = std::max(1, std::min(ncen, 2 * n_sm_));  // two CTAs per SM (SIMT and tcgen05)
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
@@ -541,7 +554,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     double t0 = 0;
     for (int i = 0; i < 16; ++i) t0 += static_cast<double>(h[i]);
     fprintf(stderr, "[nnmd phases forward] total %.3e cycles:", t0);
-    for (int i = 0; i < 8; ++i) fprintf(stderr, " %d:%.1f%%", i, 100.0 * h[i] / (t0 > 0 ? t0 : 1));
+    for (int i = 0; i < 16; ++i) fprintf(stderr, " %d:%.1f%%", i, 100.0 * h[i] / (t0 > 0 ? t0 : 1));
     fprintf(stderr, " | gemm-internal:");
     for (int i = 16; i < 24; ++i) fprintf(stderr, " g%d:%.1f%%", i - 16, 100.0 * h[i] / (t0 > 0 ? t0 : 1));
     fprintf(stderr, "\n");

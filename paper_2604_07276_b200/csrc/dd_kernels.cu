@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
   if (lane == 0) {
     a.nn[li] = cnt > a.n_max ? 0 : cnt;  // overflow: reported, list left empty
     if (a.nonempty && cnt > 0) atomicAdd(a.nonempty, 1);
+    if (a.maxn) atomicMax(a.maxn, cnt);
   }
   if (cnt > a.n_max) {
     if (lane == 0) atomicMin(a.err, ca);

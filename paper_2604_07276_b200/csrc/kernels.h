@@ -90,6 +90,7 @@ struct NbrArgs {
   int* nn;                   // [n_lists]
   int* err;                  // &err[slot]: atomicMin of the owner atom of an overflowing list
   int* nonempty;             // optional: count of lists with >= 1 row (route entries)
+  int* maxn;                 // optional: atomicMax of the row counts
 };
 void launch_neighbors(const NbrArgs& a, cudaStream_t st);
 
@@ -184,7 +185,9 @@ struct DpArgs {
   const uint8_t* img_ew[kMaxLayers];
   const uint8_t* img_ewT[kMaxLayers];
   int wimg;  // 1: all of the above are present (the per-centre kernels' WIMG variant)
+  int fwd2;  // 1: the on-chip chained forward (k_centre_forward2): wimg, M == 128, n <= 128
 };
+size_t forward2_smem_bytes(const DpArgs& a);
 // Weight images: bytes for a K x N operand, and the builder (B(k,n) = TB ? W[n*ldb+k] :
 // W[k*ldb+n]).
 size_t weight_image_bytes(int K, int N);
