@@ -530,6 +530,8 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     dp.fwd2 = h_counts_[12] <= 128 ? 1 : 0;
   }
   dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
+  work_.ensure(1);
+  dp.work = work_.p;
   const int grid = std::max(1, std::min(ncen, 2 * n_sm_));  // two CTAs per SM (SIMT and tcgen05)
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
   scratch_.ensure(dp.scratch_slot * grid);

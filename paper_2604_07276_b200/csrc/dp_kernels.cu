@@ -192,6 +192,18 @@ __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
   return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
 }
 
+// Dynamic centre scheduling for the persistent per-centre kernels: each CTA starts at
+// blockIdx.x and then takes the next unclaimed centre (costs vary with n and n^2, so a
+// static stride leaves a tail; results do not depend on the order).  `ctr` is zeroed
+// before the launch.
+__device__ int next_centre(int* ctr) {
+  __shared__ int s_next;
+  __syncthreads();
+  if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
+  __syncthreads();
+  return s_next;
+}
+
 // Stage centre c's env rows (written by k_env) into shared memory; returns sigma.
 __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int& zi) {
   zi = a.species[a.m_atom[a.cen_member[c]]];
@@ -458,7 +470,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
     }
   }
   const int M = a.M, M2 = 2 * M, mr = a.mr;
-  for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
+  for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {
     const int n = a.nn[c];
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     int zi;
@@ -696,7 +708,7 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward2(const __grid_constan
     tc::fence_after();
   };
 
-  for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
+  for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {
     const int n = a.nn[c];
     const int ln = (n + 3) & ~3;
     int zi;
@@ -1038,7 +1050,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   }
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int c = blockIdx.x; c < a.n_centres; c += gridDim.x) {
+  for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {
     const int n = a.nn[c];
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot, n);
@@ -1406,6 +1418,7 @@ static void launch_forward2(const DpArgs& a, int n_sm, cudaStream_t st) {
 template <bool FWD>
 static void launch_centre(const DpArgs& a, int grid, cudaStream_t st) {
   if (a.n_centres == 0) return;
+  cudaMemsetAsync(a.work, 0, sizeof(int), st);
   if (FWD && a.fwd2 && a.mode != 0) {
     // one CTA per SM (grid = 2 CTAs per SM for the other kernels)
     const int n_sm = (grid + 1) / 2;
