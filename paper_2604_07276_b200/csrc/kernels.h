@@ -177,7 +177,8 @@ struct DpArgs {
   size_t scratch_slot;  // floats per CTA slot
   int mode;             // 0 SIMT FP32, 1 3xTF32 tcgen05, 2 1xTF32 tcgen05
   unsigned long long* prof;  // optional per-phase cycle counters (thread 0 of each CTA)
-  int flags;            // experiment switches (NNMD_FLAGS): bit0 no L2 prefetch, bit1 unfused row pass
+  int flags;            // diagnostic switches (env NNMD_FLAGS, 0 in production): bit0 no L2 prefetch
+                        // of the stash, bit1 unfused backward n x n passes, bit2 no weight images
   // pre-split weight images (launch_weight_image) of the per-centre weight GEMMs' B
   // operands, or NULL: U = X [A|B], dX += dU [A|B]^T, embedding forward / backward
   const uint8_t* img_ab[16];
