@@ -50,11 +50,11 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-def make_system(n_gpus, weak, seed=1):
+def make_system(n_gpus, weak, seed=1, replicas=0):
     import paper_2604_07276_b200 as nb
     box, pos, sp = nb.synth_system(N_ATOMS, RHO, 0.9, seed)
-    if weak and n_gpus > 1:
-        reps = n_gpus
+    reps = replicas if replicas > 0 else (n_gpus if weak else 1)
+    if reps > 1:
         pos = np.concatenate([pos + np.array([k * box[0], 0.0, 0.0]) for k in range(reps)])
         sp = np.concatenate([sp] * reps)
         box = np.array([box[0] * reps, box[1], box[2]])
@@ -167,7 +167,7 @@ def cpu_reference_sample(box, pos, sp, rc, n_sample, seed=0):
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    box, pos, sp = make_system(args.gpus, args.weak)
+    box, pos, sp = make_system(args.gpus, args.weak, replicas=args.replicas)
     vals = []
     for i in range(args.warmup + args.steps):
         r = cpu_reference_sample(box, pos, sp, args.rc, args.ref_sample, seed=i)
@@ -211,7 +211,7 @@ def run_ours(args, ws, rank, local):
     import paper_2604_07276_b200 as nb
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    box, pos, sp = make_system(args.gpus, args.weak)
+    box, pos, sp = make_system(args.gpus, args.weak, replicas=args.replicas)
     n = len(pos)
     model = nb.init_model(nb.paper_spec(args.rc), 1)
     uid = nb.DeviceEvaluator.nccl_unique_id() if (ws > 1 and rank == 0) else None
@@ -392,6 +392,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--rc", type=float, default=6.0)
     ap.add_argument("--weak", action="store_true")
+    ap.add_argument("--replicas", type=int, default=0,
+                    help="replicate the 15,668-atom box this many times along x (cli.cpp:654-669) on the given "
+                         "GPUs; default: --gpus with --weak, else 1")
     ap.add_argument("--scheme", choices=["masked", "wide"], default="masked")
     ap.add_argument("--ref-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
