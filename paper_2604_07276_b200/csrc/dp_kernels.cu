@@ -164,6 +164,8 @@ __host__ __device__ inline size_t smem_layout(const DpArgs& a, int mode, unsigne
 }
 
 // Phase timer: thread 0 accumulates clock64 deltas per phase id when a.prof is set.
+// Compiled in only for profiling builds (make PHASES=1 -> -DNB_PHASE_PROF).
+#ifdef NB_PHASE_PROF
 struct PhaseClock {
   unsigned long long* out;
   long long last;
@@ -187,6 +189,13 @@ struct PhaseClock {
       for (int i = 0; i < 24; ++i) atomicAdd(out + i, acc[i]);
   }
 };
+#else
+struct PhaseClock {
+  __device__ __forceinline__ void start(unsigned long long*) {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void flush() {}
+};
+#endif
 
 __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
   return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
@@ -463,12 +472,14 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
   mm.init(sm.head);
   PhaseClock pc;
   pc.start(a.prof);
+#ifdef NB_PHASE_PROF
   if constexpr (MODE != 0) {
     if (a.prof && threadIdx.x == 0) {
       mm.st.prof = pc.acc + 16;
       mm.st.t_last = clock64();
     }
   }
+#endif
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {
     const int n = a.nn[c];
@@ -1042,12 +1053,14 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   mm.init(sm.head);
   PhaseClock pc;
   pc.start(a.prof);
+#ifdef NB_PHASE_PROF
   if constexpr (MODE != 0) {
     if (a.prof && threadIdx.x == 0) {
       mm.st.prof = pc.acc + 16;
       mm.st.t_last = clock64();
     }
   }
+#endif
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {

@@ -59,12 +59,16 @@ struct State {
   unsigned long long* prof;  // optional: thread 0 accumulates cycles per GEMM stage (ids 0..7)
   long long t_last;
   int dbg;  // microbenchmark switches (0 in production)
+  // Phase clock of the GEMM internals: compiled in only for profiling builds
+  // (make PHASES=1 -> -DNB_PHASE_PROF); a no-op otherwise.
   __device__ __forceinline__ void tick(int id) {
+#ifdef NB_PHASE_PROF
     if (prof && threadIdx.x == 0) {
       const long long t = clock64();
       if (id >= 0) prof[id] += static_cast<unsigned long long>(t - t_last);
       t_last = t;
     }
+#endif
   }
 };
 
