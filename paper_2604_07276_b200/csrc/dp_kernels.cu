@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward2(const __grid_constan
           }
           tc::mma_commit(&st.bar[s]);
         }
-        ++st.uses[s];
+        st.use(s);
         if (q + 1 < 8) {
           // the other stage is free once step q-1's MMAs have read it; its copy then
           // overlaps step q's MMAs
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward2(const __grid_constan
         }
         tc::mma_commit(&st.bar[0]);
       }
-      ++st.uses[0];
+      st.use(0);
       mma_wait_all();
       pc.mark(5);
       // ---- U_B^T image into XI (the X image is no longer needed): row m, K = j
@@ -952,7 +952,7 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward2(const __grid_constan
         }
         tc::mma_commit(&st.bar[0]);
       }
-      ++st.uses[0];
+      st.use(0);
       mma_wait_all();
       pc.mark(8);
       // ---- X' = X + acc: stash, and the X image of the next layer

@@ -45,6 +45,7 @@ struct alignas(1024) Smem {
 
 // Per-CTA pipeline state (identical in every thread).
 struct State {
+  uint8_t* base;        // stage buffers: A [stage][hi/lo] 16 KB each, then B 32 KB each
   uint8_t* a[2][2];
   uint8_t* b[2][2];
   uint64_t* bar;
@@ -54,8 +55,13 @@ struct State {
   uint32_t tmem;
   uint64_t* tbar;       // weight-image bulk copies
   uint32_t tph;         // bulk-copy phases consumed (thread 0)
-  uint32_t uses[2];     // commits issued per stage
-  uint32_t waited[2];   // commits waited per stage
+  // commits issued / waited per stage, as scalars so the state stays in registers
+  // (a stage index is a runtime value; an array indexed by it would live in local memory)
+  uint32_t uses0, uses1, waited0, waited1;
+  __device__ __forceinline__ void use(int s) {
+    if (s) ++uses1;
+    else ++uses0;
+  }
   unsigned long long* prof;  // optional: thread 0 accumulates cycles per GEMM stage (ids 0..7)
   long long t_last;
   int dbg;  // microbenchmark switches (0 in production)
@@ -184,6 +190,7 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int k) {
 // Allocate TMEM and initialise the barriers.  Call once per CTA, all threads.
 template <int NST>
 __device__ __forceinline__ void init(State& st, Smem<NST>* sm, int cols) {
+  st.base = &sm->a[0][0][0];
   for (int s = 0; s < 2; ++s)
     for (int p = 0; p < 2; ++p) {
       st.a[s][p] = sm->a[s % NST][p];
@@ -195,8 +202,8 @@ __device__ __forceinline__ void init(State& st, Smem<NST>* sm, int cols) {
   st.tmem_slot = &sm->tmem_base;
   st.nst = NST;
   st.cols = cols;
-  st.uses[0] = st.uses[1] = 0;
-  st.waited[0] = st.waited[1] = 0;
+  st.uses0 = st.uses1 = 0;
+  st.waited0 = st.waited1 = 0;
   st.prof = nullptr;
   st.t_last = 0;
   st.dbg = 0;
@@ -229,9 +236,16 @@ __device__ __forceinline__ void finish(State& st) {
 }
 
 __device__ __forceinline__ void wait_stage(State& st, int s) {
-  while (st.waited[s] < st.uses[s]) {
-    mbar_wait(&st.bar[s], st.waited[s] & 1u);
-    ++st.waited[s];
+  if (s) {
+    while (st.waited1 < st.uses1) {
+      mbar_wait(&st.bar[1], st.waited1 & 1u);
+      ++st.waited1;
+    }
+  } else {
+    while (st.waited0 < st.uses0) {
+      mbar_wait(&st.bar[0], st.waited0 & 1u);
+      ++st.waited0;
+    }
   }
 }
 
@@ -424,7 +438,7 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
         st.tick(4);
         if (c + 1 < nch) load(c + 1);  // next chunk's global loads overlap this chunk's MMAs
         st.tick(0);
-        ++st.uses[s];
+        st.use(s);
         if (PROMOTE > 0 && nch > PROMOTE && ((c + 1) % PROMOTE == 0 || c + 1 == nch)) {
           wait_stage(st, 0);
           wait_stage(st, 1);
@@ -457,7 +471,7 @@ __device__ __forceinline__ void gemm2(State& st, int M, int N, int K, const floa
       const uint32_t acc_col = (PROMOTE > 0 && nch > PROMOTE) ? kSumCol : 0u;
       // ---- epilogue, in column blocks of <= 128: TMEM -> registers -> shared (row-major,
       // padded) -> coalesced epi over rows
-      float* stg = reinterpret_cast<float*>(st.a[0][0]);  // operand stages are free now
+      float* stg = reinterpret_cast<float*>(st.base);  // operand stages are free now
       const int q = warp & 3;
       const int mrows = M - m0 < kMT ? M - m0 : kMT;
       for (int cb0 = 0; cb0 < NT; cb0 += 128) {
@@ -583,7 +597,7 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   constexpr bool two = NPASS > 1;
-  uint8_t* base = st.a[0][0];
+  uint8_t* base = st.base;
   const uint32_t lanes = static_cast<uint32_t>(32 * (warp & 3)) << 16;
   const int arow = 32 * (warp & 3) + lane;
   const int akof = 16 * (warp >> 2);
@@ -667,7 +681,7 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
           }
           mma_commit(&st.bar[s]);
         }
-        ++st.uses[s];
+        st.use(s);
         st.tick(4);
         if (c + 1 < nch) load(c + 1);  // next chunk's global loads overlap this chunk's MMAs
         st.tick(0);
