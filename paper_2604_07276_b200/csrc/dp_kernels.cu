@@ -64,7 +64,11 @@ __device__ inline Slot slot_of(const DpArgs& a, float* base, int n) {
 // NST = 1: the per-centre kernels (96 KB head -> two CTAs per SM hide each other's
 // latency) run the TS-mode GEMM (A in TMEM, two B stages); NST = 2: the fitting-net tiles
 // run the SS-mode GEMM with 128-row FP32 promotion.
-template <int MODE, int NST = 1>
+// TSO (tensor-core modes): every per-centre GEMM routed through run() takes the TS path
+// (N > 128 as several 128-column tiles); only run_wide() keeps the SS path for the one
+// N = 256 product.  Used by the WIMG kernels (M = 128), so no SS code is instantiated at
+// the other call sites: smaller kernels, fewer instruction-cache misses.
+template <int MODE, int NST = 1, bool TSO = false>
 struct Mm {
   GemmSmem* gs;
   tc::State st;
@@ -83,11 +87,19 @@ struct Mm {
     else if constexpr (NST == 1 && PROMOTE == 0) {
       // N > 128 would need a second A staging per 128-column tile in TS mode: the wide
       // U = X [A|B] product stays on the SS path, which covers N = 256 in one tile
-      if (N <= tc::kTsN) tc::gemm_ts<TA, TB, MODE == 1 ? 3 : 1, EK, IMG>(st, M, N, K, A, lda, B, ldb, epi, img);
+      if (TSO || N <= tc::kTsN) tc::gemm_ts<TA, TB, MODE == 1 ? 3 : 1, EK, IMG>(st, M, N, K, A, lda, B, ldb, epi, img);
       else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, 0, 1, EK, IMG>(st, M, N, K, A, lda, B, ldb, epi, img);
     } else {
       tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
     }
+  }
+  // N = 256 in one SS tile (U = X [A|B]); falls back to run() on the SIMT path.
+  template <bool TA, bool TB, bool IMG = false, class Epi>
+  __device__ __forceinline__ void run_wide(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                                           Epi epi, const uint8_t* img = nullptr) {
+    if constexpr (MODE == 0) bgemm<TA, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
+    else if (N <= tc::kTsN) tc::gemm_ts<TA, TB, MODE == 1 ? 3 : 1, 1, IMG>(st, M, N, K, A, lda, B, ldb, epi, img);
+    else tc::gemm<TA, TB, MODE == 1 ? 3 : 1, 0, 1, 1, IMG>(st, M, N, K, A, lda, B, ldb, epi, img);
   }
   // C = epi(A1 B1 + A2 B2) with one accumulator (tcgen05) or, on the SIMT path, two
   // passes through `acc` (ld N, must not alias the epilogue's sources).
@@ -230,8 +242,8 @@ __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int
 
 // Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
 // Writes intermediate activations to EMB and the last to `out` (n x M).
-template <int MODE, bool WIMG>
-__device__ void embed_forward(Mm<MODE, 1>& mm, const DpArgs& a, int n, int zi, const Smem& sm, float* emb,
+template <int MODE, bool WIMG, class MmT>
+__device__ void embed_forward(MmT& mm, const DpArgs& a, int n, int zi, const Smem& sm, float* emb,
                               float* out) {
   const int E0 = a.edims[0];
   float* cur = (a.n_embed == 1) ? out : emb;
@@ -468,7 +480,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
   Smem sm;
   smem_layout(a, MODE, dp_smem, &sm);
-  Mm<MODE> mm;
+  Mm<MODE, 1, WIMG> mm;
   mm.init(sm.head);
   PhaseClock pc;
   pc.start(a.prof);
@@ -497,7 +509,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
       float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
       float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
       float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
-      mm.template run<false, false, 0, 1, WIMG>(n, M2, M, Xl, M, a.ab[l], M2,
+      mm.template run_wide<false, false, WIMG>(n, M2, M, Xl, M, a.ab[l], M2,
                                                 [&](int k, int j, auto v) { vst(&Ul[k * M2 + j], v); }, a.img_ab[l]);
       __syncthreads();
       pc.mark(2);
@@ -1049,7 +1061,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
   Smem sm;
   smem_layout(a, MODE, dp_smem, &sm);
-  Mm<MODE> mm;
+  Mm<MODE, 1, WIMG> mm;
   mm.init(sm.head);
   PhaseClock pc;
   pc.start(a.prof);
