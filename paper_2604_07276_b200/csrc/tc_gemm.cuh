@@ -656,6 +656,9 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
         } else {
           store_chunk<!TB2, 4>(NT, fb, bh, bl, two);
         }
+        // the next chunk's global loads go out before the barrier (the stores above have
+        // already taken their source registers)
+        if (c + 1 < nch) load(c + 1);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         st.tick(2);
         fence_before();
@@ -683,8 +686,6 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
         }
         st.use(s);
         st.tick(4);
-        if (c + 1 < nch) load(c + 1);  // next chunk's global loads overlap this chunk's MMAs
-        st.tick(0);
       }
       wait_stage(st, 0);
       wait_stage(st, 1);
