@@ -662,7 +662,7 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         st.tick(2);
         fence_before();
-        fence_proxy_async();
+        if (!((IMG1 || IMG2) && img)) fence_proxy_async();  // B staged by st.shared this chunk
         __syncthreads();
         st.tick(3);
         if (tid == 0) {
