@@ -1280,11 +1280,25 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         dY = dXn;
         dXn = tmp;
       }
+      // ds_k += sum_o dU0_ko w0_o: warp per row, lanes over o (coalesced), 4 rows per
+      // warp with their loads issued together
       const int E0 = a.edims[0];
-      for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        float du = 0.f;
-        for (int o = 0; o < E0; ++o) du += dY[k * E0 + o] * a.w0[o];
-        sm.dsx[k] += du;
+      for (int k0 = wid; k0 < n; k0 += 4 * nw) {
+        float du[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int o = lane; o < E0; o += 32) {
+          const float w = a.w0[o];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = k0 + u * nw;
+            if (k < n) du[u] += dY[k * E0 + o] * w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float v = warp_sum(du[u]);
+          const int k = k0 + u * nw;
+          if (lane == 0 && k < n) sm.dsx[k] += v;
+        }
       }
       __syncthreads();
     }
