@@ -462,6 +462,119 @@ __device__ void bwd_col_pass(int n, int ln, int stride, const float* TS, int ldt
   tc::fence_proxy_async();  // part may sit in an operand stage that bulk copies overwrite later
 }
 
+// Row and column passes in one sweep over dP~ (n <= 128, blockDim <= 256): warp per query
+// row k, lane owning columns 4 lane .. 4 lane + 3 for the whole sweep.  Each warp keeps its
+// column sums (dw_j and the column gate sum_k dC_kj R_k) in registers across its rows and
+// parks them in part ([nw][128] float4 + [nw][128] float); dsigma is summed per lane and
+// reduced once.  After t_k is reduced the row's dS is written from the same registers, so
+// dP~ and pu are read once.  Same results as bwd_row_pass + bwd_col_pass up to summation
+// order.
+__device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float* __restrict__ PU, float* DS,
+                            float inv_sig, const Smem& sm, unsigned char* part_raw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float4* pg = reinterpret_cast<float4*>(part_raw);       // [nw][128]
+  float* pw = reinterpret_cast<float*>(pg + nw * 128);    // [nw][128]
+  const int j4 = 4 * lane;
+  const bool act = j4 < n;
+  float sj2[4];
+  float4 Rj[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const bool v = j4 + q < n;
+    const float sj = v ? sm.s[j4 + q] : 0.f;
+    sj2[q] = sj * sj;
+    Rj[q] = v ? sm.R[j4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float cw[4] = {0.f, 0.f, 0.f, 0.f};
+  float4 cg[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) cg[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float dsg = 0.f;
+  for (int k = wid; k < n; k += nw) {
+    const float4 Rk = sm.R[k];
+    float4 tv = make_float4(0.f, 0.f, 0.f, 0.f), pu = tv;
+    if (act) {
+      tv = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(k) * ldt + j4);
+      pu = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(k) * ln + j4);
+    }
+    const float tq[4] = {tv.x, tv.y, tv.z, tv.w};
+    float pq[4] = {pu.x, pu.y, pu.z, pu.w};
+    float dP[4];
+    float t = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool v = j4 + q < n;
+      const float tt = v ? tq[q] : 0.f;  // the tile and stash hold junk past column n
+      pq[q] = v ? pq[q] : 0.f;
+      const float C = dot4(Rk, Rj[q]);
+      const float pv = sj2[q] * pq[q];
+      dP[q] = tt * C * inv_sig;
+      const float dC = tt * pv * inv_sig;
+      dsg -= dC * C * inv_sig;
+      t += dP[q] * pv;
+      g0 += dC * Rj[q].x;
+      g1 += dC * Rj[q].y;
+      g2 += dC * Rj[q].z;
+      g3 += dC * Rj[q].w;
+      cg[q].x += dC * Rk.x;
+      cg[q].y += dC * Rk.y;
+      cg[q].z += dC * Rk.z;
+      cg[q].w += dC * Rk.w;
+    }
+    t = warp_sum(t);
+    // the row gate's four sums in 6 shuffles: halve the values per step, then a butterfly;
+    // lanes 0, 8, 16, 24 end up with components x, y, z, w
+    {
+      const bool hi16 = lane & 16;
+      float a0 = hi16 ? g2 : g0, a1 = hi16 ? g3 : g1;
+      a0 += __shfl_xor_sync(0xffffffffu, hi16 ? g0 : g2, 16);
+      a1 += __shfl_xor_sync(0xffffffffu, hi16 ? g1 : g3, 16);
+      const bool hi8 = lane & 8;
+      float b = hi8 ? a1 : a0;
+      b += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+      b += __shfl_xor_sync(0xffffffffu, b, 4);
+      b += __shfl_xor_sync(0xffffffffu, b, 2);
+      b += __shfl_xor_sync(0xffffffffu, b, 1);
+      if ((lane & 7) == 0) reinterpret_cast<float*>(&sm.dR[k])[lane >> 3] += b;
+    }
+    float ds[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float dpt = dP[q] - t;
+      cw[q] += pq[q] * dpt;
+      ds[q] = sj2[q] * pq[q] * dpt;
+    }
+    if (act) *reinterpret_cast<float4*>(DS + static_cast<size_t>(k) * ln + j4) = make_float4(ds[0], ds[1], ds[2], ds[3]);
+  }
+  dsg = warp_sum(dsg);
+  if (lane == 0) sm.red[8 + wid] = dsg;
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      pg[wid * 128 + j4 + q] = cg[q];
+      pw[wid * 128 + j4 + q] = cw[q];
+    }
+  }
+  __syncthreads();
+  float dsig = 0.f;
+  for (int w = 0; w < nw; ++w) dsig += static_cast<float>(sm.red[8 + w]);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    float dw = 0.f;
+    float4 r = sm.dR[j];
+    for (int w = 0; w < nw; ++w) {
+      const float4 p = pg[w * 128 + j];
+      r.x += p.x;
+      r.y += p.y;
+      r.z += p.z;
+      r.w += p.w;
+      dw += pw[w * 128 + j];
+    }
+    sm.dsx[j] += 2.f * sm.s[j] * (dw + dsig);
+    sm.dR[j] = r;
+  }
+  tc::fence_proxy_async();  // part sits in an operand stage that bulk copies overwrite later
+}
+
 }  // namespace
 
 size_t dp_scratch_floats(const DpArgs& a) {
@@ -1190,18 +1303,17 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
       pc.mark(2);
       // T = dP~ = dY U_B^T, then the row and column passes (bwd_row_pass, bwd_col_pass)
-      // -> dS in sl.T.  With tcgen05 and n <= 128 both passes run in the GEMM epilogue on
-      // the shared-memory accumulator tile (dP~ never goes to global memory); the column
-      // partials sit behind that tile in the same (idle) operand-stage buffer.
+      // -> dS in sl.T.  With tcgen05 and n <= 128 both passes run as one sweep
+      // (bwd_rc_pass) in the GEMM epilogue on the shared-memory accumulator tile (dP~ never
+      // goes to global memory); the per-warp column partials sit behind that tile in the
+      // same (idle) operand-stage buffer.
       bool fused_rc = false;
       if constexpr (MODE != 0) {
         if (n <= 128 && !(a.flags & 2)) {
           unsigned char* part = sm.head + kPartOff;
           mm.template run<false, true, 0, 2>(n, n, M, dY, M, Ul + M, M2,
                                              [&](const float* stg, int ldst, int, int, int, int) {
-                                               bwd_row_pass(n, ln, stg, ldst, PUl, inv_sig, sm);
-                                               __syncthreads();
-                                               bwd_col_pass(n, ln, n, stg, ldst, PUl, sl.T, inv_sig, sm, part);
+                                               bwd_rc_pass(n, ln, stg, ldst, PUl, sl.T, inv_sig, sm, part);
                                              });
           fused_rc = true;
         }
