@@ -1338,8 +1338,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       pc.mark(9);
       // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T  (both products in one accumulator)
       {
-        float* xo = dXn;
-        const float* yi = dY;
+        float* __restrict__ xo = dXn;
+        const float* __restrict__ yi = dY;
         if (l > 0) {
           mm.template run2<true, false, false, true, WIMG>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
                                                      [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&yi[k * M + m], v) + v); },
@@ -1347,7 +1347,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         } else {
           // bottom layer: the embedding's output tanh derivative (dp_core.hpp:580-583) is
           // applied in the same epilogue, dX0 (1 - X0^2)
-          const float* x0 = X;
+          const float* __restrict__ x0 = X;
           mm.template run2<true, false, false, true, WIMG>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
                                                      [=](int k, int m, auto v) {
                                                        vst(&xo[k * M + m], (vld(&yi[k * M + m], v) + v) * vdtanh(vld(&x0[k * M + m], v)));
@@ -1381,10 +1381,11 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
       for (int e = a.n_embed - 1; e >= 1; --e) {
         const int Ein = a.edims[e - 1], Eout = a.edims[e];
-        const float* h = a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride + offs[e - 1];
+        const float* __restrict__ h = a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride + offs[e - 1];
+        float* __restrict__ xo = dXn;
         mm.template run<false, false, 0, 1, WIMG>(n, Ein, Eout, dY, Eout, a.ew[e], Ein,
-                                                  [&](int k, int i, auto v) {
-                                                    vst(&dXn[k * Ein + i], v * vdtanh(vld(&h[k * Ein + i], v)));
+                                                  [=](int k, int i, auto v) {
+                                                    vst(&xo[k * Ein + i], v * vdtanh(vld(&h[k * Ein + i], v)));
                                                   },
                                                   a.img_ewT[e]);
         __syncthreads();
@@ -1448,9 +1449,26 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
           for (int b = 0; b < 3; ++b) w[3 * q + b] -= gk[q] * d[b];
         }
       }
-      for (int q = 0; q < 9; ++q) {
-        const double t = block_sum(w[q], sm.red + 8);
-        if (threadIdx.x == 0) a.vir[static_cast<size_t>(c) * 9 + q] = t;
+      // the nine sums with one barrier: warp sums, then a fixed-order sum over warps
+      // (block_sum's order, so the same bits), parked in dA's (dead) shared buffer
+      if (static_cast<size_t>(M) * 4 * sizeof(float) >= 9 * nw * sizeof(double)) {
+        double* vr = reinterpret_cast<double*>(sm.dAd);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) w[q] = warp_sum(w[q]);
+        if (lane == 0)
+#pragma unroll
+          for (int q = 0; q < 9; ++q) vr[wid * 9 + q] = w[q];
+        __syncthreads();
+        if (threadIdx.x < 9) {
+          double t = 0.0;
+          for (int v = 0; v < nw; ++v) t += vr[v * 9 + threadIdx.x];
+          a.vir[static_cast<size_t>(c) * 9 + threadIdx.x] = t;
+        }
+      } else {
+        for (int q = 0; q < 9; ++q) {
+          const double t = block_sum(w[q], sm.red + 8);
+          if (threadIdx.x == 0) a.vir[static_cast<size_t>(c) * 9 + q] = t;
+        }
       }
     }
     __syncthreads();
