@@ -217,13 +217,24 @@ __device__ __forceinline__ float dot4(const float4& a, const float4& b) {
 // blockIdx.x and then takes the next unclaimed centre (costs vary with n and n^2, so a
 // static stride leaves a tail; results do not depend on the order).  `ctr` is zeroed
 // before the launch.
-__device__ int next_centre(int* ctr) {
-  __shared__ int s_next;
-  __syncthreads();
-  if (threadIdx.x == 0) s_next = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
-  __syncthreads();
-  return s_next;
-}
+// Thread 0 claims the following centre as soon as it starts one (CentreQueue::next), so
+// the atomic's round trip overlaps the centre's work instead of sitting between centres.
+struct CentreQueue {
+  int* ctr;
+  int claimed;  // thread 0 only
+  __device__ explicit CentreQueue(int* c) : ctr(c), claimed(0) {
+    if (threadIdx.x == 0) claimed = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
+  }
+  __device__ int next() {
+    __shared__ int s_next;
+    __syncthreads();
+    if (threadIdx.x == 0) s_next = claimed;
+    __syncthreads();
+    const int c = s_next;
+    if (threadIdx.x == 0) claimed = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
+    return c;
+  }
+};
 
 // Stage centre c's env rows (written by k_env) into shared memory; returns sigma.
 __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int& zi) {
@@ -606,7 +617,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
   }
 #endif
   const int M = a.M, M2 = 2 * M, mr = a.mr;
-  for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {
+  CentreQueue queue(a.work);
+  for (int c = blockIdx.x; c < a.n_centres; c = queue.next()) {
     const int n = a.nn[c];
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     int zi;
@@ -844,7 +856,8 @@ __global__ void __launch_bounds__(256, 1) k_centre_forward2(const __grid_constan
     tc::fence_after();
   };
 
-  for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {
+  CentreQueue queue(a.work);
+  for (int c = blockIdx.x; c < a.n_centres; c = queue.next()) {
     const int n = a.nn[c];
     const int ln = (n + 3) & ~3;
     int zi;
@@ -1188,7 +1201,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
 #endif
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int c = blockIdx.x; c < a.n_centres; c = next_centre(a.work)) {
+  CentreQueue queue(a.work);
+  for (int c = blockIdx.x; c < a.n_centres; c = queue.next()) {
     const int n = a.nn[c];
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot, n);
