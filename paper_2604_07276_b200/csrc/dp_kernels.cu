@@ -1266,9 +1266,11 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
     for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
       const int k = idx / M, m = idx - k * M;
       const float* R = reinterpret_cast<const float*>(&sm.R[k]);
-      float v = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) v += sm.dAd[m * 4 + cc] * R[cc];
+      const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];  // one conflict-free 16-byte read
+      float v = da.x * R[0];
+      v += da.y * R[1];
+      v += da.z * R[2];
+      v += da.w * R[3];
       if (m < mr)
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) v += sm.dBd[cc * mr + m] * R[cc];
@@ -1280,10 +1282,11 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
 #pragma unroll 4
       for (int m = lane; m < M; m += 32) {
         const float x = Xf[k * M + m];
-        v0 += x * sm.dAd[m * 4 + 0];
-        v1 += x * sm.dAd[m * 4 + 1];
-        v2 += x * sm.dAd[m * 4 + 2];
-        v3 += x * sm.dAd[m * 4 + 3];
+        const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];
+        v0 += x * da.x;
+        v1 += x * da.y;
+        v2 += x * da.z;
+        v3 += x * da.w;
         if (m < mr) {
           v0 += x * sm.dBd[0 * mr + m];
           v1 += x * sm.dBd[1 * mr + m];
