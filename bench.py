@@ -16,10 +16,16 @@
 * e2e      = steps/s through the C-ABI host entry point (nnmd_b200_compute) from pinned
              host buffers: H2D of coords/types/gids and D2H of energy/virial/forces/
              per-atom energies inside the timed region (wall clock, max over ranks).
-* reference arm (--impl reference) = the compiled reference (oracle/_ref) on this box's
-             host cores: build_neighbor_list + a bounded sample of centres through
-             center_rows + evaluate_center (fwd + exact bwd) on all host threads,
-             extrapolated to the whole system (rank 0 only).
+* reference arm (--impl reference) = the compiled reference (oracle/_ref, built from the
+             unmodified sources) on this box's host cores, rank 0 only, inputs from the
+             oracle's own generator (no product library in that process).  One FULL
+             force evaluation is timed, tiled over the K timed steps: step i runs the
+             reference's per-step work for centres [i*n/K, (i+1)*n/K) --
+             build_neighbor_list + the stock evaluate_dp with a LocalMask, split over all
+             host threads.  value = 1 / (mean list build + sum of the K slice
+             evaluations), i.e. full steps/s; the whole timed region is one full step.
+* --gpus N without WORLD_SIZE in the environment re-launches itself under
+             torch.distributed.run (N ranks, 127.0.0.1); NCCL_DEBUG=INFO goes to stderr.
 """
 import argparse
 import json
@@ -50,9 +56,16 @@ def host_threads():
         return os.cpu_count() or 1
 
 
-def make_system(n_gpus, weak, seed=1, replicas=0):
-    import paper_2604_07276_b200 as nb
-    box, pos, sp = nb.synth_system(N_ATOMS, RHO, 0.9, seed)
+def make_system(n_gpus, weak, seed=1, replicas=0, oracle_gen=False):
+    """configs[1] system (replicated along x for weak scaling, cli.cpp:654-669).  The
+    reference arm uses the oracle's generator (bitwise equal, tests/test_oracle.py) so
+    that its process never maps the product library."""
+    if oracle_gen:
+        import oracle as O
+        box, pos, sp = O.Port().synth_system(N_ATOMS, RHO, 0.9, seed)
+    else:
+        import paper_2604_07276_b200 as nb
+        box, pos, sp = nb.synth_system(N_ATOMS, RHO, 0.9, seed)
     reps = replicas if replicas > 0 else (n_gpus if weak else 1)
     if reps > 1:
         pos = np.concatenate([pos + np.array([k * box[0], 0.0, 0.0]) for k in range(reps)])
@@ -148,7 +161,8 @@ def bcast_bytes(b, ws):
 
 # ---------------------------------------------------------------------------------------
 def cpu_reference_sample(box, pos, sp, rc, n_sample, seed=0):
-    """Compiled reference on host cores: neighbour list + n_sample centres (fwd+bwd)."""
+    """cpu_baseline leg of our arm: compiled reference on host cores, neighbour list +
+    n_sample random centres (center_rows + evaluate_center, fwd+bwd), extrapolated."""
     import oracle as O
     R = O.Ref()
     spec = dict(O.PAPER_SPEC, rc=rc, rcs=0.55 * rc, n_max=O.nmax_for_rc(rc))
@@ -164,25 +178,56 @@ def cpu_reference_sample(box, pos, sp, rc, n_sample, seed=0):
                        f"(center_rows+evaluate_center, fwd+bwd) on {threads} threads, extrapolated x{len(pos)/len(centres):.1f}")
 
 
+def workload_config(args, n, ws):
+    """The config dict both arms print (the driver compares them)."""
+    return {"workload": f"1HCI-sized synthetic solvated protein, {n} atoms, DPA-1 1.58M params, rc={args.rc} A, "
+                        f"{'weak' if args.weak else 'strong'} DD over {args.gpus} GPU(s)",
+            "n_atoms": n, "rc": args.rc, "n_max": {4.0: 64, 6.0: 160, 8.0: 320}.get(float(args.rc), 160),
+            "dd_ranks": args.gpus, "scheme": args.scheme, "model_seed": 1, "system_seed": 1,
+            "l2": "flushed between steps (256 MB write)"}
+
+
 def run_reference(args, ws, rank):
+    """The reference's own CPU implementation on this box's host cores (rank 0 only)."""
     if rank != 0:
         return
-    box, pos, sp = make_system(args.gpus, args.weak, replicas=args.replicas)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference_sample(box, pos, sp, args.rc, args.ref_sample, seed=i)
-        if i >= args.warmup:
-            vals.append(r["value"])
-    v = float(np.median(vals))
+    import oracle as O
+    box, pos, sp = make_system(args.gpus, args.weak, replicas=args.replicas, oracle_gen=True)
+    n = len(pos)
+    R = O.Ref()
+    spec = dict(O.PAPER_SPEC, rc=args.rc, rcs=0.55 * args.rc, n_max=O.nmax_for_rc(args.rc))
+    h = R.model_init(spec, 1)
+    threads = host_threads()
+    for i in range(args.warmup):  # untimed: a few centres to fault in code, weights and pages
+        R.step_slice(h, pos, sp, box, (i * 97) % (n - 8), (i * 97) % (n - 8) + 8, threads)
+    K = max(1, args.steps)
+    bounds = [n * i // K for i in range(K + 1)]
+    t_list, t_eval, e_sum = [], [], 0.0
+    for i in range(K):
+        if bounds[i + 1] <= bounds[i]:
+            continue
+        tl, te, e = R.step_slice(h, pos, sp, box, bounds[i], bounds[i + 1], threads)
+        t_list.append(tl)
+        t_eval.append(te)
+        e_sum += e
+    R.model_free(h)
+    t_step = float(np.mean(t_list)) + float(np.sum(t_eval))
+    v = 1.0 / t_step
+    sample = (f"one full force evaluation of all {n} centres, tiled over the {K} timed steps (step i = "
+              f"build_neighbor_list + stock evaluate_dp with a LocalMask over centres [i*n/K, (i+1)*n/K) on "
+              f"{threads} host threads); value = 1 / (mean list build + sum of slice evaluations)")
     line = {"impl": "reference", "metric": "MD steps/s (DPA-1 force evaluation per step)", "value": v,
             "unit": "steps/s", "higher_is_better": True, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 / v, "ns_per_day": ns_per_day(v),
+            "warmup": args.warmup, "ms_per_step": 1000.0 * t_step, "ns_per_day": ns_per_day(v),
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic solvated protein (nnmd_synth_system), random-init DPA-1 weights",
-            "config": {"workload": f"1HCI-sized {len(pos)} atoms, DPA-1 1.58M params, rc={args.rc}",
-                       "n_atoms": len(pos), "rc": args.rc},
-            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": r["cores"], "kind": "reference",
-                             "sample": r["sample"]},
+            "data": "synthetic solvated protein (oracle synth_system seed 1 == nnmd_synth_system), "
+                    "random-init DPA-1 weights (reference init_model seed 1)",
+            "config": workload_config(args, n, ws),
+            "timed_region_s": float(np.sum(t_list) + np.sum(t_eval)),
+            "full_steps_timed": 1,
+            "t_list_s_mean": float(np.mean(t_list)), "t_eval_s_sum": float(np.sum(t_eval)),
+            "energy": e_sum,
+            "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -276,10 +321,14 @@ def run_ours(args, ws, rank, local):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    peak = peaks.get("bf16_tflops_sustained", 1366.3)
-    traffic = None
-    try:  # DRAM bytes per launch of the dominant kernel from the latest ncu --set full capture
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_latest.json")))["k_centre_backward"]["dram_bytes"]
+    # the kernel is timed per launch at full clock (no power cap seen): burst peak
+    peak = peaks.get("bf16_tflops", 1622.5)
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+        nc = json.load(open(os.path.join(ROOT, "profiles", "ncu_latest.json")))
+        traffic = nc["k_centre_backward"]["dram_bytes"]
+        traffic_src = ("profiles/ncu_latest.json: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                       f"ncu --set full capture ({nc.get('_source', 'earlier run')}), not this run")
     except Exception:
         pass
     achieved = f_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0
@@ -354,21 +403,19 @@ def run_ours(args, ws, rank, local):
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
             "dtype": {"fp32": "f32 (3xTF32 tcgen05)", "tf32": "tf32", "simt": "f32 (SIMT)"}[args.precision], "data": "synthetic solvated protein (nnmd_synth_system seed 1), random-init DPA-1 weights (init_model seed 1)",
+            "nccl": nccl_info(ws),
             "ns_per_day": ns_per_day(value),
-            "config": {"workload": f"1HCI-sized solvated protein, {n} atoms, DPA-1 1.58M params, rc={args.rc} A, "
-                                   f"{'weak' if args.weak else 'strong'} DD over {ws} GPU(s)",
-                       "n_atoms": n, "rc": args.rc, "n_max": nb.paper_spec(args.rc).n_max,
-                       "dd_ranks": ws, "scheme": args.scheme, "l2": "flushed between steps (256 MB write)",
-                       "precision": {"fp32": "3xTF32 tcgen05 (FP32-grade, tol 1e-5)", "tf32": "1xTF32 tcgen05 (tol 2e-3)",
-                                     "simt": "FP32 SIMT (tol 1e-5)"}[args.precision] + "; fp64 geometry/forces"},
+            "config": dict(workload_config(args, n, ws),
+                           precision={"fp32": "3xTF32 tcgen05 (FP32-grade, tol 1e-5)", "tf32": "1xTF32 tcgen05 (tol 5e-3)",
+                                      "simt": "FP32 SIMT (tol 1e-5)"}[args.precision] + "; fp64 geometry/forces"),
             "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ns_per_day": ns_per_day(e2e)},
             "roofline": {"bound": "tensor", "kernel": "k_centre_backward", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_flop_per_launch": f_bwd, "ms_per_launch": k_bwd,
                          "executed_tflops": npass * x_bwd / (k_bwd * 1e-3) / 1e12 if k_bwd > 0 else 0.0,
                          "mma_passes": npass,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; kernel timed per launch)",
                          "forward": {"ms_per_launch": k_fwd, "algorithmic_flop": f_fwd,
                                      "achieved_tflops": f_fwd / (k_fwd * 1e-3) / 1e12 if k_fwd > 0 else 0.0}},
             "hbm_kernels": hbm,
@@ -382,6 +429,23 @@ def run_ours(args, ws, rank, local):
         }
         print(json.dumps(line), flush=True)
     ev.close()
+
+
+def nccl_info(ws):
+    """What NCCL reported at communicator init (NCCL_DEBUG=INFO), for the rank count check."""
+    return {"world_size": ws, "NCCL_DEBUG": os.environ.get("NCCL_DEBUG"),
+            "debug_file": os.environ.get("NCCL_DEBUG_FILE"), "backend": "nccl" if ws > 1 else "none (1 process)"}
+
+
+def respawn_under_torchrun(n):
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) ourselves."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -401,7 +465,16 @@ def main():
     ap.add_argument("--precision", choices=["fp32", "tf32", "simt"], default="fp32",
                     help="fp32 = 3xTF32 tcgen05 (FP32-grade, default); tf32 = 1xTF32 tcgen05; simt = CUDA-core FP32")
     args = ap.parse_args()
+    # NCCL init lines ("... rank r nranks N ... Init COMPLETE") to stderr; stdout keeps the
+    # one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(respawn_under_torchrun(args.gpus))
     ws, rank, local = dist_setup()
+    if ws != args.gpus and args.impl == "ours":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {ws}")
     if args.impl == "reference":
         run_reference(args, ws, rank)
     else:

@@ -49,7 +49,7 @@ enum { NNMD_MASKED_REDUCTION = 0, NNMD_WIDE_HALO = 1 };
  * forces, energies and virial are FP64):
  *   NNMD_PREC_FP32      3xTF32 on tcgen05 tensor cores (hi/lo split) -- FP32-grade,
  *                       parity tolerance 1e-5 relative (default)
- *   NNMD_PREC_TF32      1xTF32 on tcgen05 -- stated tolerance 2e-3 relative
+ *   NNMD_PREC_TF32      1xTF32 on tcgen05 -- stated tolerance 5e-3 relative
  *   NNMD_PREC_FP32_SIMT plain FP32 FMA on CUDA cores (validation path) -- 1e-5 */
 enum { NNMD_PREC_FP32 = 0, NNMD_PREC_TF32 = 1, NNMD_PREC_FP32_SIMT = 2 };
 
@@ -88,16 +88,22 @@ void nnmd_b200_destroy(nnmd_b200* ctx);
 nnmd_status nnmd_b200_nccl_unique_id(void* out128);
 
 /* DpProvider::evaluate / dd_evaluate with HOST buffers (positions must be wrapped into
- * [0, L) on periodic axes).  Outputs are the replicated full-system results:
- * energy = sum of owned per-atom energies, forces[3n] = -dE/dx, virial[9] row-major
+ * [0, L) on periodic axes; with world_size > 1 only world rank 0's coords are read -- the
+ * others may pass NULL -- and reach every GPU by ncclBroadcast, collective 1).  Outputs are
+ * the replicated full-system results: energy = sum of owned per-atom energies, forces[3n] = -dE/dx, virial[9] row-major
  * W_ab = -sum g_{k,a} d_{k,b}, atom_energy[n] (NULL to skip). */
 nnmd_status nnmd_b200_compute(nnmd_b200* ctx, int64_t n, const double* coords,
                               const int32_t* types, const int64_t* gids, const double box[3],
                               const uint8_t periodic[3], double* energy, double* forces,
                               double* virial, double* atom_energy);
 
-/* Same evaluation on DEVICE-resident inputs/outputs (pointers on ctx's device); no host
- * copies, no host synchronisation beyond the single capacity read-back of the DD build.
+/* Same evaluation on DEVICE-resident inputs/outputs (pointers on ctx's device); no bulk
+ * host copies.  Host synchronisation points per call: one per DD rank handled by this
+ * process (the locals/ghosts count read-back that sizes the rank's buffers; wide_halo adds
+ * a second for the centre count) and one at the end (step flags: overflow / wrap errors
+ * and route counts, all-reduced over processes so that every process throws together).
+ * The call returns with the stream idle.  With world_size > 1 the positions of world
+ * rank 0 are broadcast to all processes (collective 1) before the DD build.
  * d_out layout (float64): [energy, virial(9), forces(3n), atom_energy(n)]. */
 nnmd_status nnmd_b200_compute_device(nnmd_b200* ctx, int64_t n, const double* d_coords,
                                      const int32_t* d_types, const int64_t* d_gids,
@@ -119,7 +125,9 @@ typedef struct {
  * replicated copy, so no position collective is needed.  coords/velocities are updated in
  * place; potential[k] / total[k] (may be NULL) receive run_md's per-step potential energy
  * and potential + on-step kinetic energy (mid-point velocities).  A non-finite force fails
- * with NNMD_ERROR "run_md: non-finite force from provider 'nnmd_b200' at step k". */
+ * with NNMD_ERROR "run_md: non-finite force from provider 'nnmd_b200' at step k" before
+ * that step integrates (engine.cpp:166-176): coords/velocities hold the failing step's
+ * state. */
 nnmd_status nnmd_b200_run_md(nnmd_b200* ctx, int64_t n, double* coords, double* velocities,
                              const double* masses, const int32_t* types, const int64_t* gids,
                              const double box[3], const uint8_t periodic[3], const nnmd_md_config* cfg,

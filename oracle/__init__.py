@@ -163,6 +163,9 @@ class Ref(_Lib):
         L.ref_time_centers.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, _ip, C.c_int, C.c_int, _dp, _dp, _dp]
         L.ref_fd_force_component.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, C.c_int, C.c_int, C.c_double, _dp]
         L.ref_evaluate_center_rows.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _ip, _dp, _dp]
+        L.ref_evaluate_dp_mt.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, C.c_int, _dp, _dp, _dp, _dp]
+        L.ref_step_slice.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, C.c_int, C.c_int, C.c_int,
+                                     _dp, _dp, _dp]
 
     def set_nmax(self, h, n_max):
         self.lib.ref_model_set_nmax(h, n_max)
@@ -192,6 +195,27 @@ class Ref(_Lib):
         w = np.zeros(9) if virial else None
         self._chk(self.lib.ref_evaluate_dp(h, *self._sysargs(pos, species, gids, box, periodic), C.byref(e), _d(f), _d(ae), _d(w)))
         return dict(energy=e.value, forces=f, atom_energy=ae, virial=None if w is None else w.reshape(3, 3))
+
+    def evaluate_mt(self, h, pos, species, box, workers, gids=None, periodic=None):
+        """evaluate_dp on `workers` threads; bitwise equal to evaluate() (ref_capi.cpp)."""
+        pos, species, gids, box, periodic = self._sys(pos, species, gids, box, periodic)
+        n = len(pos)
+        e = C.c_double()
+        f = np.zeros((n, 3))
+        ae = np.zeros(n)
+        w = np.zeros(9)
+        self._chk(self.lib.ref_evaluate_dp_mt(h, *self._sysargs(pos, species, gids, box, periodic), workers,
+                                              C.byref(e), _d(f), _d(ae), _d(w)))
+        return dict(energy=e.value, forces=f, atom_energy=ae, virial=w.reshape(3, 3))
+
+    def step_slice(self, h, pos, species, box, c0, c1, workers, gids=None, periodic=None):
+        """Reference per-step work for centres [c0, c1): build_neighbor_list + stock
+        evaluate_dp with a LocalMask on `workers` threads.  -> (t_list s, t_eval s, E)."""
+        pos, species, gids, box, periodic = self._sys(pos, species, gids, box, periodic)
+        tl, te, es = C.c_double(), C.c_double(), C.c_double()
+        self._chk(self.lib.ref_step_slice(h, *self._sysargs(pos, species, gids, box, periodic), c0, c1, workers,
+                                          C.byref(tl), C.byref(te), C.byref(es)))
+        return tl.value, te.value, es.value
 
     def center_rows(self, h, pos, species, box, gids=None, periodic=None, cap=None):
         pos, species, gids, box, periodic = self._sys(pos, species, gids, box, periodic)
@@ -281,7 +305,16 @@ class Port(_Lib):
         L.orc_partition_ranks.argtypes = [_dp, C.c_int, C.c_double, _ip]
         L.orc_owner_ranks.argtypes = [C.c_int, _dp, _dp, _ip, _ip]
         L.orc_build_halo.argtypes = [C.c_int, _dp, _dp, _u8p, _ip, C.c_int, C.c_double, C.c_long, _ip, _ip, _ip, _lp]
+        L.orc_synth_system.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_uint64, _dp, _dp, _ip]
         L.orc_dd_rank.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _lp]
+
+    def synth_system(self, n, rho=0.1, min_sep=0.9, seed=1):
+        """Synthetic solvated-protein input (box, pos[n,3], species[n]); == nnmd_synth_system."""
+        box = np.zeros(3)
+        pos = np.zeros((n, 3))
+        sp = np.zeros(n, dtype=np.int32)
+        self._chk(self.lib.orc_synth_system(n, rho, min_sep, seed, _d(box), _d(pos), _i(sp)))
+        return box, pos, sp
 
     def flat(self, h):
         n = self.nparams(h)

@@ -63,6 +63,10 @@ int orc_dd_rank(const orc_model* m, int n, const double* pos, const int* species
                 int n_ranks, int scheme, int rank, double* forces, double* atom_energy,
                 double* energy, double* virial, long* stats);
 
+/* Synthetic solvated-protein input (bitwise equal to nnmd_synth_system). */
+int orc_synth_system(int64_t n, double rho, double min_sep, uint64_t seed, double* box,
+                     double* pos, int32_t* types);
+
 #ifdef __cplusplus
 }
 #endif

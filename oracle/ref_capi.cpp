@@ -332,6 +332,118 @@ int ref_time_centers(void* m, int n, const double* pos, const int* species,
   });
 }
 
+// evaluate_dp (deeppot.cpp:315-369) with the per-centre work spread over `workers` host
+// threads: each thread runs the public center_rows + evaluate_center on an interleaved
+// share of the centres; the force assembly then replays evaluate_dp's loop order
+// (ForceAccumulator adds in ascending centre order, deeppot.cpp:351-362) so E, F and e_i
+// are bitwise identical to the single-threaded evaluate_dp.  The virial is
+// summed in the same centre order.  Golden-vector generation for the big configs only.
+int ref_evaluate_dp_mt(void* m, int n, const double* pos, const int* species,
+                       const int64_t* gids, const double* box3, const uint8_t* periodic,
+                       int workers, double* energy, double* forces, double* atom_energy,
+                       double* virial) {
+  return guarded([&] {
+    const DPModel& model = M(m);
+    model.validate();
+    AtomSet atoms = make_atoms(n, pos, species, gids);
+    SimBox box = make_box(box3, periodic);
+    box.validate(model.rc);
+    const NeighborList list = build_neighbor_list(atoms, box, model.rc, ListMode::full);
+    std::vector<std::vector<EnvRow>> rows(static_cast<std::size_t>(n));
+    std::vector<CenterGrads> cgs(static_cast<std::size_t>(n));
+    std::atomic<int> next{0};
+    const int nw = std::max(workers, 1);
+    std::vector<std::exception_ptr> errs(static_cast<std::size_t>(nw));
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nw; ++w)
+      pool.emplace_back([&, w] {
+        try {
+          auto ws = new_workspace();
+          for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1)) {
+            rows[i] = center_rows(i, list, atoms, box, model);
+            cgs[i] = evaluate_center(model, atoms.species[i], rows[i], *ws, true);
+          }
+        } catch (...) {
+          errs[w] = std::current_exception();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    ForceAccumulator acc(static_cast<std::size_t>(n));
+    double e = 0.0, w9[9] = {0};
+    for (int i = 0; i < n; ++i) {
+      const CenterGrads& cg = cgs[i];
+      if (atom_energy) atom_energy[i] = cg.energy;
+      e += cg.energy;
+      acc.add(i, kZeroShift, cg.center_grad);
+      for (std::size_t k = 0; k < rows[i].size(); ++k) {
+        acc.add(rows[i][k].member, rows[i][k].image, cg.row_grads[k]);
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b) w9[3 * a + b] -= cg.row_grads[k][a] * rows[i][k].d[b];
+      }
+    }
+    const auto f = acc.finalize();
+    *energy = e;
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < 3; ++a) forces[3 * i + a] = f[i][a];
+    if (virial) std::memcpy(virial, w9, sizeof w9);
+  });
+}
+
+// Reference-arm step slice (bench.py --impl reference): the reference's own per-step
+// work for the centres [c0, c1) -- build_neighbor_list (neighbor.cpp:73-148), then the
+// stock evaluate_dp (deeppot.cpp:315-369) with a LocalMask selecting that slice, split
+// over `workers` host threads (one evaluate_dp call per thread on an equal sub-slice,
+// like run_rank_tasks' per-rank threads, decomp.cpp:233-256) and the per-thread force
+// arrays summed.  Seconds for the list build and for the evaluation are returned apart
+// so a full step = one list build + the K slices that tile [0, n).
+int ref_step_slice(void* m, int n, const double* pos, const int* species,
+                   const int64_t* gids, const double* box3, const uint8_t* periodic,
+                   int c0, int c1, int workers, double* t_list, double* t_eval,
+                   double* energy_sum) {
+  return guarded([&] {
+    const DPModel& model = M(m);
+    AtomSet atoms = make_atoms(n, pos, species, gids);
+    SimBox box = make_box(box3, periodic);
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    const NeighborList list = build_neighbor_list(atoms, box, model.rc, ListMode::full);
+    const auto t1 = clk::now();
+    require(0 <= c0 && c0 < c1 && c1 <= n, "ref_step_slice: bad centre range");
+    const int nw = std::max(1, std::min(workers, c1 - c0));
+    std::vector<DpResult> res(static_cast<std::size_t>(nw));
+    std::vector<std::exception_ptr> errs(static_cast<std::size_t>(nw));
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nw; ++w)
+      pool.emplace_back([&, w] {
+        try {
+          const long span = c1 - c0;
+          const int a = c0 + static_cast<int>(span * w / nw), b = c0 + static_cast<int>(span * (w + 1) / nw);
+          LocalMask mask;
+          mask.owned.assign(static_cast<std::size_t>(n), 0);
+          for (int i = a; i < b; ++i) mask.owned[i] = 1;
+          res[w] = evaluate_dp(atoms, box, list, model, &mask);
+        } catch (...) {
+          errs[w] = std::current_exception();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    std::vector<Vec3> f(static_cast<std::size_t>(n));
+    double e = 0.0;
+    for (const auto& r : res) {
+      e += r.energy;
+      for (int i = 0; i < n; ++i) f[i] += r.forces[i];
+    }
+    const auto t2 = clk::now();
+    *t_list = std::chrono::duration<double>(t1 - t0).count();
+    *t_eval = std::chrono::duration<double>(t2 - t1).count();
+    *energy_sum = e;
+  });
+}
+
 // tests/support.hpp fd_force_component: central FD of the total DP energy.
 int ref_fd_force_component(void* m, int n, const double* pos, const int* species,
                            const int64_t* gids, const double* box3, const uint8_t* periodic,

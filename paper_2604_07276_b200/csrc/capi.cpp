@@ -44,7 +44,7 @@ nb::Context& C(nnmd_b200* h) {
 extern "C" {
 
 const char* nnmd_b200_last_error(void) { return g_err.c_str(); }
-const char* nnmd_b200_version(void) { return "nnmd_b200 0.1 (sm_100a, fp32 SIMT network, fp64 geometry)"; }
+const char* nnmd_b200_version(void) { return "nnmd_b200 0.2 (sm_100a, 3xTF32 tcgen05 network, fp64 geometry/forces)"; }
 
 nnmd_status nnmd_model_init(const nnmd_model_spec* spec, uint64_t seed, nnmd_model** out) {
   return guarded([&] {
@@ -156,7 +156,8 @@ nnmd_status nnmd_b200_compute(nnmd_b200* h, int64_t n, const double* coords, con
                               const int64_t* gids, const double box[3], const uint8_t periodic[3],
                               double* energy, double* forces, double* virial, double* atom_energy) {
   return guarded([&] {
-    nb::require(box && (n == 0 || (coords && types)), "nnmd_b200_compute: null argument");
+    // coords may be NULL on world ranks > 0 (positions arrive by the collective-1 broadcast)
+    nb::require(box && (n == 0 || types), "nnmd_b200_compute: null argument");
     const uint8_t per_default[3] = {1, 1, 1};
     C(h).compute_host(n, coords, types, gids, box, periodic ? periodic : per_default, energy, forces,
                       virial, atom_energy);

@@ -3,9 +3,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace nb {
 
 constexpr int kWarp = 32;
+
+// Max-dynamic-SMEM attribute of a kernel, raised on demand per (device, kernel): the
+// attribute is per device, and the size a launch needs can grow (n_max).
+inline void ensure_smem_attr(const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, func}];
+  if (smem > have) {
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    have = smem;
+  }
+}
 
 // Packed image shift: (sx+1)*9 + (sy+1)*3 + (sz+1), 13 == zero shift.
 __host__ __device__ inline int pack_shift(int sx, int sy, int sz) {

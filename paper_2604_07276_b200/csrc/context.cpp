@@ -119,6 +119,7 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   CU(cudaMemcpy(weights_.p, wh_.blob.data(), wh_.blob.size() * sizeof(float), cudaMemcpyHostToDevice));
   build_weight_images();
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_counts_), 64 * sizeof(int)));
+  CU(cudaMallocHost(reinterpret_cast<void**>(&h_flags_), (kFlagWords + 64) * sizeof(int)));
   require(o.n_ranks <= 48, "nnmd_b200: at most 48 DD ranks");
   stats_.resize(static_cast<size_t>(o.n_ranks));
   debug_.resize(static_cast<size_t>(o.n_ranks));
@@ -148,6 +149,7 @@ Context::~Context() {
   for (auto e : md_ev_)
     if (e) cudaEventDestroy(e);
   if (h_counts_) cudaFreeHost(h_counts_);
+  if (h_flags_) cudaFreeHost(h_flags_);
   if (h_out_) cudaFreeHost(h_out_);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -222,26 +224,47 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
     sys.L[a] = box[a];
     sys.per[a] = periodic[a] ? 1 : 0;
   }
+  // collective 1 (gather_positions, decomp.cpp:157-186, 285-296): every process takes the
+  // positions of world rank 0 (ncclBroadcast of f64 [n][3]); ids and types are static
+  if (bcast_positions()) {
+    bpos_.ensure(3 * static_cast<size_t>(n) + 3);
+    tic("nccl_broadcast");
+    const Nccl& N = nccl();
+    const int rc = N.Broadcast(d_pos, bpos_.p, 3 * static_cast<size_t>(n), kNcclFloat64, 0, comm_, st_);
+    if (rc != 0) throw CudaError(std::string("ncclBroadcast: ") + N.GetErrorString(rc));
+    toc();
+    sys.pos = bpos_.p;
+  }
   tic("owner");
   launch_owner(sys, dims.data(), owner_.p, err_.p, st_);
   toc();
+  // step flags: [0, 8) = -err (so a max-reduction keeps the lowest failing atom), [8, 8+R)
+  // = ghost-route entries of each DD rank (written by its owning process only)
+  flags_.ensure(kFlagWords + opts_.n_ranks);
+  CU(cudaMemsetAsync(flags_.p, 0, (kFlagWords + opts_.n_ranks) * sizeof(int), st_));
   for (int r = 0; r < opts_.n_ranks; ++r)
     if (r % opts_.world_size == opts_.world_rank) run_rank(r, sys, dims.data(), thickness, d_out, keep_debug_);
+  launch_negate(err_.p, flags_.p, kFlagWords, st_);
   if (use_nccl_) {
+    // collective 2 (reduce_forces, decomp.cpp:188-204, 471-538): [E, W, F, e_i] summed
+    // over processes; then the error words and route counts, so that every process sees
+    // an overflow on any rank and all of them throw together
     tic("nccl_allreduce");
     const Nccl& N = nccl();
-    const int rc = N.AllReduce(d_out, d_out, out_len, kNcclFloat64, kNcclSum, comm_, st_);
+    int rc = N.AllReduce(d_out, d_out, out_len, kNcclFloat64, kNcclSum, comm_, st_);
+    if (rc == 0) rc = N.AllReduce(flags_.p, flags_.p, kFlagWords + opts_.n_ranks, kNcclInt32, kNcclMax, comm_, st_);
     if (rc != 0) throw CudaError(std::string("ncclAllReduce: ") + N.GetErrorString(rc));
     toc();
   }
-  CU(cudaMemcpyAsync(h_counts_ + 8, err_.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CU(cudaMemcpyAsync(h_flags_, flags_.p, (kFlagWords + opts_.n_ranks) * sizeof(int), cudaMemcpyDeviceToHost, st_));
   CU(cudaStreamSynchronize(st_));
   collect_times();
   if (opts_.scheme == NNMD_MASKED_REDUCTION)
-    for (int r = 0; r < opts_.n_ranks; ++r)
-      if (r % opts_.world_size == opts_.world_rank) stats_[static_cast<size_t>(r)].counts[3] = h_counts_[16 + (r % 48)];
+    for (int r = 0; r < opts_.n_ranks; ++r) stats_[static_cast<size_t>(r)].counts[3] = h_flags_[kFlagWords + r];
   if (use_nccl_) {
-    const double comm = ktimes_.back().second;
+    double comm = 0;
+    for (const auto& kt : ktimes_)
+      if (kt.first.rfind("nccl_", 0) == 0) comm += kt.second;
     for (auto& s : stats_) s.ms[3] += comm;
   }
   if (trace_on_ || ledger_on_) {
@@ -250,8 +273,9 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
       if (r % opts_.world_size == opts_.world_rank) local.push_back(r);
     record_trace(n, local);
   }
-  if (h_counts_[9] != 0x7f7f7f7f || h_counts_[10] != 0x7f7f7f7f) {
-    const int atom = std::min(h_counts_[9], h_counts_[10]);
+  const int ovf0 = -h_flags_[1], ovf1 = -h_flags_[2];
+  if (ovf0 != 0x7f7f7f7f || ovf1 != 0x7f7f7f7f) {
+    const int atom = std::min(ovf0, ovf1);
     int64_t gid = atom;
     if (d_gid) CU(cudaMemcpy(&gid, d_gid + atom, sizeof gid, cudaMemcpyDeviceToHost));
     int own = 0;
@@ -655,9 +679,8 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   launch_energy_virial(e_.p, vir_.p, counts_.p, d_out, st_);
   toc();
   phases_.push_back({rank, 3, ph_f0, timers_.size() - 1});
-  if (!wide) {
-    CU(cudaMemcpyAsync(h_counts_ + 16 + (rank % 48), counts_.p + 3, sizeof(int), cudaMemcpyDeviceToHost, st_));
-  }
+  if (!wide)
+    CU(cudaMemcpyAsync(flags_.p + kFlagWords + rank, counts_.p + 3, sizeof(int), cudaMemcpyDeviceToDevice, st_));
 
   if (keep_debug) {
     CU(cudaStreamSynchronize(st_));
@@ -721,7 +744,12 @@ void Context::compute_host(long n, const double* pos, const int* types, const in
   gid_.ensure(static_cast<size_t>(n) + 1);
   out_.ensure(10 + 4 * static_cast<size_t>(n));
   if (n) {
-    CU(cudaMemcpyAsync(pos_.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st_));
+    // with the position broadcast only world rank 0's coordinates are used (others may pass
+    // NULL): collective 1 replaces the replicated host input
+    if (coords_needed()) {
+      require(pos != nullptr, "nnmd_b200_compute: null coordinates on world rank 0");
+      CU(cudaMemcpyAsync(pos_.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st_));
+    }
     CU(cudaMemcpyAsync(types_.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st_));
     if (gid) {
       CU(cudaMemcpyAsync(gid_.p, gid, n * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
@@ -805,6 +833,7 @@ void Context::record_trace(long n, const std::vector<int>& local_ranks) {
     for (const auto& t : timers_) {
       if (t.name == "owner") owner = &t;
       if (t.name == "nccl_allreduce") nccl = &t;
+      if (t.name == "nccl_broadcast") owner = &t;  // collective 1 proper when there is one
     }
     if (owner) spans_.push_back({-1, 1, ev_time(owner->a), ev_time(owner->b), step_});
     double f0 = 1e300, f1 = -1e300;
@@ -826,8 +855,10 @@ void Context::record_trace(long n, const std::vector<int>& local_ranks) {
   if (ledger_on_) {
     ledger_.push_back({step_, 0, static_cast<uint64_t>(n) * 20u, R});
     if (masked) {
+      // route counts of every DD rank (all-reduced with the step flags), as dd_evaluate
+      // records the total over all R ranks (decomp.cpp:463-468)
       uint64_t routed = 0;
-      for (int r : local_ranks) routed += static_cast<uint64_t>(stats_[static_cast<size_t>(r)].counts[3]);
+      for (int r = 0; r < R; ++r) routed += static_cast<uint64_t>(stats_[static_cast<size_t>(r)].counts[3]);
       ledger_.push_back({step_, 1, routed * 20u, R});
     }
     ledger_.push_back({step_, 2, static_cast<uint64_t>(n) * 12u, R});
@@ -889,11 +920,14 @@ void Context::run_md(long n, double* d_pos, double* d_vel, const double* d_mass,
       throw Error("run_md: non-finite force from provider 'nnmd_b200' at step " + std::to_string(bad));
   };
   for (long step = 0; step < cfg.n_steps; ++step) {
-    if (step > 0) check_forces();  // the previous step's forces were finite
     // forces of the current positions (replicated on every process after the all-reduce,
     // so each process integrates its own copy: no position collective is needed)
     compute_device(n, d_pos, d_types, d_gid, box, periodic, out_.p);
     ma.step = static_cast<int>(step);
+    // run_md (engine.cpp:166-176) rejects non-finite forces BEFORE integrating: the state
+    // is left at the failing step
+    launch_force_check(ma, st_);
+    check_forces();
     if (trace_on_) CU(cudaEventRecord(md_ev_[0], st_));
     launch_leapfrog(ma, st_);
     launch_energy_record(md_ke_.p, ma.n, out_.p, d_rec, step, st_);
@@ -908,7 +942,7 @@ void Context::run_md(long n, double* d_pos, double* d_vel, const double* d_mass,
     }
     ++step_;
   }
-  check_forces();
+  CU(cudaStreamSynchronize(st_));
 }
 
 void Context::run_md_host(long n, double* pos, double* vel, const double* mass, const int* types,
@@ -937,7 +971,17 @@ void Context::run_md_host(long n, double* pos, double* vel, const double* mass, 
     CU(cudaMemcpyAsync(types_.p, types, n * sizeof(int), cudaMemcpyHostToDevice, st_));
     CU(cudaMemcpyAsync(gid_.p, gid, n * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
   }
-  run_md(n, pos_.p, md_vel_.p, md_mass_.p, types_.p, gid_.p, box, periodic, cfg, md_rec_.p);
+  try {
+    run_md(n, pos_.p, md_vel_.p, md_mass_.p, types_.p, gid_.p, box, periodic, cfg, md_rec_.p);
+  } catch (const Error&) {
+    // like the reference, leave the caller's atoms at the failing step's state
+    if (n) {
+      CU(cudaMemcpyAsync(pos, pos_.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+      CU(cudaMemcpyAsync(vel, md_vel_.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+      CU(cudaStreamSynchronize(st_));
+    }
+    throw;
+  }
   std::vector<double> rec(2 * static_cast<size_t>(cfg.n_steps));
   if (cfg.n_steps) CU(cudaMemcpyAsync(rec.data(), md_rec_.p, rec.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
   if (n) {

@@ -108,6 +108,9 @@ class Context {
  private:
   void run_rank(int rank, const SysArgs& sys, const int dims[3], double thickness, double* d_out,
                 bool keep_debug);
+  bool bcast_positions() const { return use_nccl_; }
+  bool coords_needed() const { return !bcast_positions() || opts_.world_rank == 0; }
+  static constexpr int kFlagWords = 8;
   void tic(const char* name);
   void toc();
   void collect_times();
@@ -135,7 +138,9 @@ class Context {
   DevBuf<double> md_vel_, md_mass_, md_ke_, md_rec_, md_sum_;
   DevBuf<int> md_err_;
   // step-global
-  DevBuf<int> owner_, err_;
+  DevBuf<int> owner_, err_, flags_;
+  DevBuf<double> bpos_;  // broadcast positions (collective 1)
+  int* h_flags_ = nullptr;  // pinned, kFlagWords + n_ranks
   // per rank (reused across virtual ranks)
   DevBuf<int> is_local_, gcount_, loc_off_, gh_off_, counts_;
   DevBuf<int> m_atom_, m_shift_, m_owner_, m_cell_, cflag_, coff_, cen_member_, cidx_;

@@ -39,6 +39,15 @@ __global__ void k_owner(SysArgs s, int dx, int dy, int dz, int* __restrict__ own
   if (bad) atomicMin(&err[0], i);
 }
 
+__global__ void k_negate(const int* __restrict__ src, int* __restrict__ dst, int n) {
+  const int i = threadIdx.x;
+  if (i < n) dst[i] = -src[i];
+}
+
+void launch_negate(const int* src, int* dst, int n, cudaStream_t st) {
+  k_negate<<<1, 32, 0, st>>>(src, dst, n); count_launch();
+}
+
 void launch_owner(const SysArgs& s, const int dims[3], int* owner, int* err, cudaStream_t st) {
   if (s.n == 0) return;
   k_owner<<<(s.n + 255) / 256, 256, 0, st>>>(s, dims[0], dims[1], dims[2], owner, err); count_launch();
@@ -364,11 +373,7 @@ void launch_neighbors(const NbrArgs& a, cudaStream_t st) {
   if (a.n_lists == 0) return;
   const int cap = ((a.n_max + 1 + 31) / 32) * 32;
   const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_neighbors, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(k_neighbors), smem);
   k_neighbors<<<(a.n_lists + kNbrWarps - 1) / kNbrWarps, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
 }
 

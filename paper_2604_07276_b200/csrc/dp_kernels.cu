@@ -1579,24 +1579,15 @@ void launch_env(const DpArgs& a, cudaStream_t st) {
 
 template <int MODE, bool WIMG>
 static void set_smem(size_t smem) {
-  static size_t done = 0;
-  if (smem > done) {
-    cudaFuncSetAttribute(k_centre_forward<MODE, WIMG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaFuncSetAttribute(k_centre_backward<MODE, WIMG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    done = smem;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_forward<MODE, WIMG>), smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_backward<MODE, WIMG>), smem);
 }
 
 // a.wimg: every weight GEMM has a pre-split image (tensor-core modes) -> the WIMG kernels
 template <int NPASS>
 static void launch_forward2(const DpArgs& a, int n_sm, cudaStream_t st) {
   const size_t smem = forward2_smem_bytes(a);
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(k_centre_forward2<NPASS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    set = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_forward2<NPASS, true>), smem);
   k_centre_forward2<NPASS, true><<<n_sm, 256, smem, st>>>(a);
   count_launch();
 }
@@ -1669,11 +1660,7 @@ static void fit_gemm(int M, int N, int K, const float* A, const float* B, int ld
   constexpr int TM = MODE == 0 ? kTM : tc::kMT;
   constexpr int TN = MODE == 0 ? kTN : tc::kNT;
   const size_t smem = head_bytes(MODE, 2) + 1024;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(k_fit_gemm<TB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    set = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(k_fit_gemm<TB, MODE>), smem);
   dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM);
   k_fit_gemm<TB, MODE><<<grid, 256, smem, st>>>(M, N, K, A, B, ldb, C, bias, Y, epi);
   count_launch();

@@ -37,6 +37,8 @@ void launch_dd_flags(const SysArgs& s, const RankArgs& r, const int* owner, int*
                      int* gcount, cudaStream_t st);
 // exclusive scan of n ints; out[n] receives the total (out has n+1 entries)
 void launch_scan(const int* in, int* out, int n, cudaStream_t st);
+// dst[i] = -src[i], i < n <= 32 (error words -> max-reducible step flags)
+void launch_negate(const int* src, int* dst, int n, cudaStream_t st);
 void launch_dd_members(const SysArgs& s, const RankArgs& r, const int* owner, const int* loc_off,
                        const int* gh_off, int n_atoms, int* m_atom, int* m_shift, double* m_pos,
                        int* m_owner, cudaStream_t st);
@@ -234,6 +236,8 @@ struct MdArgs {
   int step;
 };
 void launch_leapfrog(const MdArgs& a, cudaStream_t st);
+// err = step when a force component is non-finite (checked before integrating)
+void launch_force_check(const MdArgs& a, cudaStream_t st);
 // rec[2 step] = epot[0], rec[2 step + 1] = epot[0] + sum(ke_atom)  (deterministic)
 void launch_energy_record(const double* ke_atom, int n, const double* epot, double* rec, long step,
                           cudaStream_t st);

@@ -42,6 +42,13 @@ __global__ void k_leapfrog(MdArgs a) {
   if (!finite) atomicMin(a.err, a.step);
 }
 
+// err = step if any force component is non-finite (run_md's check, engine.cpp:166-176,
+// which throws before the integrator touches the atoms)
+__global__ void k_force_check(int n3, const double* __restrict__ F, int* __restrict__ err, int step) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n3 && !isfinite(F[i])) atomicMin(err, step);
+}
+
 // ke_atom[i] = 0.5 m |v|^2 of the stored velocities (kinetic_energy, engine.cpp:102-107)
 __global__ void k_kinetic(int n, const double* __restrict__ vel, const double* __restrict__ mass,
                           double* __restrict__ ke_atom) {
@@ -87,6 +94,12 @@ __global__ void k_rescale(int n, double* __restrict__ vel, const double* __restr
 void launch_leapfrog(const MdArgs& a, cudaStream_t st) {
   if (a.n == 0) return;
   k_leapfrog<<<(a.n + 255) / 256, 256, 0, st>>>(a);
+  count_launch();
+}
+
+void launch_force_check(const MdArgs& a, cudaStream_t st) {
+  if (a.n == 0) return;
+  k_force_check<<<(3 * a.n + 255) / 256, 256, 0, st>>>(3 * a.n, a.F, a.err, a.step);
   count_launch();
 }
 

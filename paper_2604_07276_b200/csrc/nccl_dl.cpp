@@ -24,9 +24,13 @@ const Nccl& nccl() {
         sym("ncclAllReduce"));
     n.Broadcast = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t)>(
         sym("ncclBroadcast"));
+    n.Send = reinterpret_cast<int (*)(const void*, size_t, int, int, NcclComm, cudaStream_t)>(sym("ncclSend"));
+    n.Recv = reinterpret_cast<int (*)(void*, size_t, int, int, NcclComm, cudaStream_t)>(sym("ncclRecv"));
+    n.GroupStart = reinterpret_cast<int (*)()>(sym("ncclGroupStart"));
+    n.GroupEnd = reinterpret_cast<int (*)()>(sym("ncclGroupEnd"));
     n.GetErrorString = reinterpret_cast<const char* (*)(int)>(sym("ncclGetErrorString"));
-    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllReduce && n.Broadcast &&
-           n.GetErrorString;
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllReduce && n.Broadcast && n.Send &&
+           n.Recv && n.GroupStart && n.GroupEnd && n.GetErrorString;
     if (!n.ok) n.err = "libnccl.so.2 is missing required symbols";
   });
   return n;

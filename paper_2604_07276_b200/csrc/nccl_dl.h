@@ -21,12 +21,20 @@ struct Nccl {
   int (*CommDestroy)(NcclComm) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
   int (*Broadcast)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*Send)(const void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
 };
 
 // ncclDataType_t / ncclRedOp_t values (nccl.h)
+constexpr int kNcclInt32 = 2;
+constexpr int kNcclInt64 = 4;
 constexpr int kNcclFloat64 = 8;
+constexpr int kNcclUint8 = 1;
 constexpr int kNcclSum = 0;
+constexpr int kNcclMax = 2;
 
 const Nccl& nccl();
 

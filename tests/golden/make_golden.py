@@ -14,6 +14,19 @@ Inputs:
 * paper_small: the paper-sized DPA-1 (1,584,945 params, seed 1, rc 6, n_max 160) on a
   400-atom synthetic solvated system (nnmd_synth_system, rho 0.1, min-sep 0.9, seed 7).
 * overflow_atom7: test_deeppot.cpp:94-103 (n_max 2, "atom id 7").
+* headline configs (BASELINE.json configs[0..1, 4]), paper-sized DPA-1, seed 1,
+  inputs from the oracle's synthetic generator (Port.synth_system, rho 0.1, min-sep 0.9),
+  which is pinned bitwise to nnmd_synth_system -- the inputs themselves are pinned by a
+  sha256 and regenerated at test time:
+    c0_1500   1,500 atoms, rc 6 (seed 2): evaluate_dp E/F/e_i/W + rows, dd_evaluate R=8
+              masked and wide (E, F, e_i, stats)
+    c1_15668  15,668 atoms, rc 6 (seed 1, the bench system): evaluate_dp E/F/e_i/W +
+              rows, dd_evaluate R=8 masked
+    rc4_2000  2,000 atoms, rc 4, n_max 64 (seed 5) and rc8_4200  4,200 atoms, rc 8,
+              n_max 320 (seed 5): evaluate_dp E/F/e_i/W + rows
+  Rows are stored as per-centre counts plus a sha256 of the canonical row table
+  (member, image x/y/z as int32, centre order) -- see rows_digest().
+  The big evaluate_dp runs use ref_evaluate_dp_mt, bitwise equal to evaluate_dp.
 """
 import hashlib
 import os
@@ -95,7 +108,55 @@ def overflow_case(R):
     print("overflow:", msg)
 
 
+def rows_digest(counts, member, image):
+    """sha256 over int32 counts[n] || int32 [sum(counts), 4] rows (member, image xyz)."""
+    rows = np.concatenate([np.asarray(member, np.int32).reshape(-1, 1), np.asarray(image, np.int32).reshape(-1, 3)], 1)
+    return hashlib.sha256(np.asarray(counts, np.int32).tobytes() + np.ascontiguousarray(rows).tobytes()).hexdigest()
+
+
+def input_digest(box, pos, sp):
+    return hashlib.sha256(np.asarray(box, np.float64).tobytes() + np.asarray(pos, np.float64).tobytes()
+                          + np.asarray(sp, np.int32).tobytes()).hexdigest()
+
+
+HEADLINE = {  # name: (n_atoms, synth seed, rc, dd runs)
+    "c0_1500": (1500, 2, 6.0, ((8, 0), (8, 1))),
+    "c1_15668": (15668, 1, 6.0, ((8, 0),)),
+    "rc4_2000": (2000, 5, 4.0, ()),
+    "rc8_4200": (4200, 5, 8.0, ()),
+}
+
+
+def headline(R, name, workers=8):
+    import time
+    n, seed, rc, dds = HEADLINE[name]
+    box, pos, sp = O.Port().synth_system(n, 0.1, 0.9, seed)
+    spec = dict(O.PAPER_SPEC, rc=rc, rcs=0.55 * rc, n_max=O.nmax_for_rc(rc))
+    h = R.model_init(spec, 1)
+    t0 = time.time()
+    res = R.evaluate_mt(h, pos, sp, box, workers)
+    counts, mem, img, d = R.center_rows(h, pos, sp, box)
+    g = dict(n=n, seed=seed, rc=rc, n_max=spec["n_max"], input_sha256=input_digest(box, pos, sp),
+             energy=res["energy"], forces=res["forces"], atom_energy=res["atom_energy"], virial=res["virial"],
+             row_counts=counts, rows_sha256=rows_digest(counts, mem, img))
+    for nr, scheme in dds:
+        tag = ("masked", "wide")[scheme]
+        dd = R.dd_evaluate(h, pos, sp, box, nr, scheme, workers=workers)
+        g[f"dd_{tag}_R{nr}_energy"] = dd["energy"]
+        g[f"dd_{tag}_R{nr}_forces"] = dd["forces"]
+        g[f"dd_{tag}_R{nr}_atom_energy"] = dd["atom_energy"]
+        g[f"dd_{tag}_R{nr}_stats"] = dd["stats"]
+    R.model_free(h)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **g)
+    print(name, n, "atoms rc", rc, "E =", res["energy"], "rows", int(counts.sum()), f"{time.time() - t0:.0f} s")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # python make_golden.py c0_1500 c1_15668 ...
+        R = O.Ref()
+        for name in sys.argv[1:]:
+            headline(R, name)
+        sys.exit(0)
     R = O.Ref()
     for i in range(3):
         dd_case(R, i)

@@ -212,7 +212,21 @@ def test_nccl_collective_path_single_gpu(monkeypatch):
     r1 = ev.compute(g["pos"], g["species"], g["box"])
     assert r1["energy"] == r0["energy"]
     assert np.array_equal(r1["forces"], r0["forces"])
-    assert any(name == "nccl_allreduce" for name, _ in ev.kernel_times())
+    names = [name for name, _ in ev.kernel_times()]
+    assert "nccl_allreduce" in names and "nccl_broadcast" in names  # collectives 2 and 1
+    # the step flags travel through the int32 max all-reduce: overflow still names the atom
+    go = load_golden("overflow_atom7")
+    mo = nb.init_model(nb.test_spec(1.5, 2, 0), 12345)
+    mo.set_n_max(2)
+    evo = nb.DeviceEvaluator(mo, n_ranks=2)
+    with pytest.raises(nb.CapacityError, match="atom id 7"):
+        evo.compute(go["pos"], go["species"], go["box"], gids=go["gids"])
+    # the ledger's ghost-route bytes are the total over all DD ranks (decomp.cpp:463-468)
+    ev.set_trace(spans=False, ledger=True)
+    ev.compute(g["pos"], g["species"], g["box"])
+    routes = sum(ev.rank_stats(k)["route_entries"] for k in range(2))
+    led = {kind: b for _, kind, b, _ in ev.ledger()}
+    assert led["ghost_force_route"] == 20 * routes and routes > 0
 
 
 @pytest.mark.parametrize("prec", [nb.PREC_FP32, nb.PREC_FP32_SIMT])

@@ -127,3 +127,47 @@ def test_oracle_matches_live_reference(port, ref):
     assert np.abs(a["forces"] - b["forces"]).max() <= 1e-12 * np.abs(a["forces"]).max()
     ref.model_free(hr)
     port.model_free(hp)
+
+
+HEADLINE = ["c0_1500", "c1_15668", "rc4_2000", "rc8_4200"]
+
+
+def test_oracle_synth_matches_product_generator(port):
+    """The oracle's synthetic generator (used by the goldens and bench.py's reference arm,
+    which must not map the product library) is bitwise the product's nnmd_synth_system."""
+    import paper_2604_07276_b200 as nb
+    for n, seed in ((15668, 1), (1500, 2), (400, 7), (37, 3)):
+        a = port.synth_system(n, 0.1, 0.9, seed)
+        b = nb.synth_system(n, 0.1, 0.9, seed)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("name", HEADLINE)
+def test_headline_golden_rows_and_sampled_centres(port, name):
+    """Headline-config goldens (compiled reference): the oracle reproduces the input
+    digest, the canonical rows (sha256 + counts) and, for sampled centres, the reference's
+    per-centre energies (bitwise-level)."""
+    import hashlib
+    g = load_golden(name)
+    box, pos, sp = port.synth_system(int(g["n"]), 0.1, 0.9, int(g["seed"]))
+    sha = hashlib.sha256(box.tobytes() + pos.tobytes() + sp.astype(np.int32).tobytes()).hexdigest()
+    assert sha == str(g["input_sha256"])
+    rc = float(g["rc"])
+    h = port.model_init(dict(O.PAPER_SPEC, rc=rc, rcs=0.55 * rc, n_max=int(g["n_max"])), 1)
+    counts, mem, img, d = port.neighbor_rows(h, pos, sp, box)
+    assert np.array_equal(counts, g["row_counts"])
+    rows = np.concatenate([mem.reshape(-1, 1), img], 1).astype(np.int32)
+    assert hashlib.sha256(counts.astype(np.int32).tobytes() + rows.tobytes()).hexdigest() == str(g["rows_sha256"])
+    off = np.concatenate([[0], np.cumsum(counts)])
+    for c in (0, len(pos) // 3, len(pos) - 1):
+        r = slice(off[c], off[c + 1])
+        e, _ = port.evaluate_center(h, int(sp[c]), d[r], sp[mem[r]])
+        assert abs(e - g["atom_energy"][c]) <= 1e-13 * max(1.0, abs(e)), (c, e, g["atom_energy"][c])
+    # golden self-consistency: E = sum e_i, net force ~ 0, W symmetric (A19)
+    assert abs(g["atom_energy"].sum() - float(g["energy"])) <= 1e-9 * abs(float(g["energy"]))
+    fmax = np.abs(g["forces"]).max()
+    assert np.abs(g["forces"].sum(axis=0)).max() <= 1e-9 * fmax * len(pos)
+    W = g["virial"]
+    assert np.abs(W - W.T).max() <= 1e-9 * np.abs(W).max()
+    port.model_free(h)
