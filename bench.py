@@ -467,7 +467,7 @@ def main():
     args = ap.parse_args()
     # NCCL init lines ("... rank r nranks N ... Init COMPLETE") to stderr; stdout keeps the
     # one JSON line
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ["NCCL_DEBUG"] = "INFO"  # (the boxes preset VERSION)
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

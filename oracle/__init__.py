@@ -163,6 +163,10 @@ class Ref(_Lib):
         L.ref_time_centers.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, _ip, C.c_int, C.c_int, _dp, _dp, _dp]
         L.ref_fd_force_component.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, C.c_int, C.c_int, C.c_double, _dp]
         L.ref_evaluate_center_rows.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _ip, _dp, _dp]
+        L.ref_fit_throughput.argtypes = [C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.ref_predict_throughput.argtypes = [C.c_double, C.c_double, C.c_double, _dp]
+        L.ref_scaling_efficiency.argtypes = [C.c_int, _ip, _dp, C.c_int, C.c_int, _dp]
+        L.ref_throughput_per_day.argtypes = [C.c_long, C.c_double, C.c_double, _dp]
         L.ref_evaluate_dp_mt.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, C.c_int, _dp, _dp, _dp, _dp]
         L.ref_step_slice.argtypes = [C.c_void_p, C.c_int, _dp, _ip, _i64p, _dp, _u8p, C.c_int, C.c_int, C.c_int,
                                      _dp, _dp, _dp]
@@ -195,6 +199,34 @@ class Ref(_Lib):
         w = np.zeros(9) if virial else None
         self._chk(self.lib.ref_evaluate_dp(h, *self._sysargs(pos, species, gids, box, periodic), C.byref(e), _d(f), _d(ae), _d(w)))
         return dict(energy=e.value, forces=f, atom_energy=ae, virial=None if w is None else w.reshape(3, 3))
+
+    # -- analysis.cpp (Eq. 8 model, efficiencies) and engine.cpp throughput_per_day
+    def fit_throughput(self, points):
+        n = len(points)
+        npa = np.ascontiguousarray([p[0] for p in points], dtype=np.float64)
+        tra = np.ascontiguousarray([p[1] for p in points], dtype=np.float64)
+        a, b, r2 = C.c_double(), C.c_double(), C.c_double()
+        res = np.zeros(n)
+        self._chk(self.lib.ref_fit_throughput(n, _d(npa), _d(tra), C.byref(a), C.byref(b), C.byref(r2), _d(res)))
+        return {"alpha": a.value, "beta": b.value, "r_squared": r2.value, "residuals": list(res)}
+
+    def predict_throughput(self, alpha, beta, n_p):
+        out = C.c_double()
+        self._chk(self.lib.ref_predict_throughput(alpha, beta, n_p, C.byref(out)))
+        return out.value
+
+    def scaling_efficiency(self, tr, reference, weak=False):
+        keys = sorted(tr)
+        npa = np.ascontiguousarray(keys, dtype=np.int32)
+        tra = np.ascontiguousarray([tr[k] for k in keys], dtype=np.float64)
+        eff = np.zeros(len(keys))
+        self._chk(self.lib.ref_scaling_efficiency(len(keys), _i(npa), _d(tra), reference, int(weak), _d(eff)))
+        return dict(zip(keys, eff.tolist()))
+
+    def throughput_per_day(self, n_steps, dt, elapsed):
+        out = C.c_double()
+        self._chk(self.lib.ref_throughput_per_day(n_steps, dt, elapsed, C.byref(out)))
+        return out.value
 
     def evaluate_mt(self, h, pos, species, box, workers, gids=None, periodic=None):
         """evaluate_dp on `workers` threads; bitwise equal to evaluate() (ref_capi.cpp)."""

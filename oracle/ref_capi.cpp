@@ -11,6 +11,7 @@
 // bench.py's reference arm / cpu_baseline leg.  Never by the product path.
 
 #include <atomic>
+#include <map>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -19,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "nnmd/analysis.hpp"
 #include "nnmd/decomp.hpp"
 #include "nnmd/deeppot.hpp"
 #include "nnmd/engine.hpp"
@@ -442,6 +444,38 @@ int ref_step_slice(void* m, int n, const double* pos, const int* species,
     *t_eval = std::chrono::duration<double>(t2 - t1).count();
     *energy_sum = e;
   });
+}
+
+// analysis.cpp:148-208 -- the Eq. 8 throughput model and the scaling efficiencies, for
+// pinning the sweep harness (paper_2604_07276_b200/sweep.py).
+int ref_fit_throughput(int n, const double* n_p, const double* tr, double* alpha, double* beta,
+                       double* r2, double* residuals) {
+  return guarded([&] {
+    std::vector<std::pair<double, double>> pts;
+    for (int i = 0; i < n; ++i) pts.emplace_back(n_p[i], tr[i]);
+    const ScalingFit f = fit_throughput(pts);
+    *alpha = f.alpha;
+    *beta = f.beta;
+    *r2 = f.r_squared;
+    for (std::size_t i = 0; i < f.residuals.size(); ++i) residuals[i] = f.residuals[i];
+  });
+}
+
+int ref_predict_throughput(double alpha, double beta, double n_p, double* out) {
+  return guarded([&] { *out = predict_throughput(alpha, beta, n_p); });
+}
+
+int ref_scaling_efficiency(int n, const int* n_p, const double* tr, int reference, int weak, double* eff) {
+  return guarded([&] {
+    std::map<int, double> m;
+    for (int i = 0; i < n; ++i) m[n_p[i]] = tr[i];
+    const auto e = scaling_efficiency(m, reference, weak != 0);
+    for (int i = 0; i < n; ++i) eff[i] = e.at(n_p[i]);
+  });
+}
+
+int ref_throughput_per_day(long n_steps, double dt, double elapsed, double* out) {
+  return guarded([&] { *out = throughput_per_day(n_steps, dt, elapsed); });
 }
 
 // tests/support.hpp fd_force_component: central FD of the total DP energy.

@@ -360,12 +360,36 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
     if (lane == 0) atomicMin(a.err, ca);
     return;
   }
+  // rank sort on the unique key: each lane ranks its (up to kPer) entries against one
+  // broadcast read of every entry, so the shared-memory sweep is done once per warp
+  // instead of once per entry
   int* out = a.nlist + static_cast<size_t>(li) * a.n_max;
-  for (int i = lane; i < cnt; i += 32) {
-    const NbrEntry me = buf[i];
-    int rank = 0;
-    for (int j = 0; j < cnt; ++j) rank += key_less(buf[j], me);
-    out[rank] = me.member;
+  constexpr int kPer = 6;  // lanes own entries lane, lane + 32, ... (n_max <= 192)
+  if (cnt <= 32 * kPer) {
+    NbrEntry mine[kPer];
+    int rank[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      rank[u] = 0;
+      if (lane + 32 * u < cnt) mine[u] = buf[lane + 32 * u];
+    }
+    const int nu = (cnt + 31) >> 5;  // warp-uniform
+    for (int j = 0; j < cnt; ++j) {
+      const NbrEntry o = buf[j];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (u < nu) rank[u] += key_less(o, mine[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+      if (lane + 32 * u < cnt) out[rank[u]] = mine[u].member;
+  } else {
+    for (int i = lane; i < cnt; i += 32) {
+      const NbrEntry me = buf[i];
+      int rank = 0;
+      for (int j = 0; j < cnt; ++j) rank += key_less(buf[j], me);
+      out[rank] = me.member;
+    }
   }
 }
 
