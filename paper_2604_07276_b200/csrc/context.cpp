@@ -544,15 +544,6 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     }
     dp.wimg = all ? 1 : 0;
   }
-  // on-chip chained forward (experimental, opt-in with NNMD_FWD2=1): needs
-  // the weight images, M = 128 and every centre's n <= 128 (one host read-back of the
-  // largest row count).  Measured slower than the two-CTA forward (14.6 vs 9.2 ms).
-  static const bool fwd2_on = getenv("NNMD_FWD2") && getenv("NNMD_FWD2")[0] == '1';
-  if (fwd2_on && dp.wimg && M == 128 && m.na >= 1 && opts_.precision != NNMD_PREC_FP32_SIMT) {
-    CU(cudaMemcpyAsync(h_counts_ + 12, maxn_.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
-    CU(cudaStreamSynchronize(st_));
-    dp.fwd2 = h_counts_[12] <= 128 ? 1 : 0;
-  }
   dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
   work_.ensure(1);
   dp.work = work_.p;

@@ -726,458 +726,6 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
 }
 
 // ------------------------------------------------------------------------------------
-// Forward, on-chip chained (one CTA per SM, all 512 TMEM columns): for n <= 128 rows and
-// M = 128 the attention layers never leave the SM between GEMMs.
-//
-//   TMEM  T0 [0,128)   U_A accumulator -> U_A hi -> P~ hi         (TS A operand)
-//         T1 [128,256) U_B accumulator -> PV accumulator
-//         T2 [256,384) U_A lo -> P~ lo
-//         T3 [384,512) S accumulator
-//   SMEM  XI  8 x 16 KB: K-major SW128 hi/lo image of X (rows k, K = m; the A operand of
-//             U = X [A|B] AND the B operand of S = U_A X^T), later of U_B^T (rows m,
-//             K = j; the B operand of X' = X + P~ U_B)
-//         WS  2 x 32 KB: [A|B] weight-image stages (TMA bulk copies), N = 128 halves
-//
-// Per layer: U (8 TMA+MMA steps, double-buffered) -> U_A split in TMEM, U stashed ->
-// S (TS) -> weighted softmax + gate by rows straight from TMEM, P~ into TMEM, U_B^T image
-// -> PV (TS) -> X' = X + acc, stashed, and re-imaged into XI for the next layer.  Only the
-// stash (U, pu, P~, X) and the layer input rows (L2) touch global memory.
-// ------------------------------------------------------------------------------------
-namespace fwd2 {
-
-constexpr int kHead = ((static_cast<int>(sizeof(tc::Smem<1>)) + 1023) / 1024) * 1024;
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])),
-      "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
-      "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
-      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])),
-      "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
-      : "memory");
-}
-
-struct Layout {
-  uint8_t* xi[8];  // [chunk][hi/lo]
-  uint8_t* ws[2];  // weight stages: hi 16 KB | lo 16 KB
-  uint64_t* wb;    // [2] bulk-copy barriers of the weight stages
-  float* red;      // [2][128] softmax row partials
-  float4* part;    // [2][128] descriptor partials
-};
-
-// Split 32 consecutive K values of one row into the hi/lo images of chunk `ch` (K-major
-// SW128, rows of 32 fp32).
-__device__ __forceinline__ void image_row32(const Layout& L, int ch, int row, const float (&v)[32]) {
-  uint8_t* hi = L.xi[2 * ch];
-  uint8_t* lo = L.xi[2 * ch + 1];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    tc::st_split(hi, lo, tc::sw128_off(row, 4 * q), x, true);
-  }
-}
-
-}  // namespace fwd2
-
-template <int NPASS, bool WIMG>
-__global__ void __launch_bounds__(256, 1) k_centre_forward2(const __grid_constant__ DpArgs a) {
-  using namespace fwd2;
-  extern __shared__ __align__(1024) unsigned char f2_raw[];
-  unsigned char* base = f2_raw + ((1024 - (tc::smem_u32(f2_raw) & 1023)) & 1023);
-  Layout L;
-  L.ws[0] = base;
-  L.ws[1] = base + 32768;
-  L.xi[0] = base + 65536;
-  L.xi[1] = base + 65536 + 16384;
-  for (int i = 2; i < 8; ++i) L.xi[i] = base + kHead + (i - 2) * 16384;
-  unsigned char* misc = base + kHead + 6 * 16384;
-  // misc: wb[2] | red[256] f32 | part[256] float4 | Smem fields (R, s, z, Ad, Bd, red64)
-  L.wb = reinterpret_cast<uint64_t*>(misc);
-  L.red = reinterpret_cast<float*>(misc + 64);
-  L.part = reinterpret_cast<float4*>(misc + 64 + 1024);
-  unsigned char* mp = misc + 64 + 1024 + 4096;
-  Smem sm{};
-  sm.head = base;
-  sm.R = reinterpret_cast<float4*>(mp);
-  mp += sizeof(float4) * a.n_max;
-  sm.s = reinterpret_cast<float*>(mp);
-  mp += ((sizeof(float) * a.n_max + 15) / 16) * 16;
-  sm.z = reinterpret_cast<int*>(mp);
-  mp += ((sizeof(int) * a.n_max + 15) / 16) * 16;
-  sm.Ad = reinterpret_cast<float*>(mp);
-  mp += sizeof(float) * a.M * 4;
-  sm.Bd = reinterpret_cast<float*>(mp);
-  mp += ((sizeof(float) * 4 * a.mr + 15) / 16) * 16;
-  sm.red = reinterpret_cast<double*>(mp);
-
-  constexpr int MODE = NPASS == 3 ? 1 : 2;
-  Mm<MODE> mm;
-  mm.init(base, 512);
-  if (threadIdx.x == 32) {
-    tc::mbar_init(&L.wb[0], 1);
-    tc::mbar_init(&L.wb[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  uint32_t wph[2] = {0, 0};  // weight-stage bulk-copy phases consumed (thread 0)
-  PhaseClock pc;
-  pc.start(a.prof);
-  tc::State& st = mm.st;
-  const uint32_t T0 = st.tmem, T1 = st.tmem + 128, T2 = st.tmem + 256, T3 = st.tmem + 384;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int row = 32 * (warp & 3) + lane;  // this thread's TMEM lane / tile row
-  const int h2 = warp >> 2;                // column half: [64 h2, 64 h2 + 64)
-  const uint32_t lanes = static_cast<uint32_t>(32 * (warp & 3)) << 16;
-  const int M = a.M, M2 = 2 * M, mr = a.mr;
-  const int nm4 = (a.n_max + 3) & ~3;
-  auto mma_wait_all = [&]() {
-    tc::wait_stage(st, 0);
-    tc::wait_stage(st, 1);
-    tc::fence_after();
-  };
-
-  CentreQueue queue(a.work);
-  for (int c = blockIdx.x; c < a.n_centres; c = queue.next()) {
-    const int n = a.nn[c];
-    const int ln = (n + 3) & ~3;
-    int zi;
-    const double sig = centre_rows(a, c, n, sm, zi);
-    const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
-    float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
-    pc.mark(0);
-    embed_forward<MODE, WIMG>(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, X);
-    __syncthreads();
-    pc.mark(1);
-    // X image of the embedding output (rows >= n zero)
-    {
-      float v[32];
-      for (int ch = 2 * h2; ch < 2 * h2 + 2; ++ch) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (row < n) x = *reinterpret_cast<const float4*>(X + row * M + 32 * ch + 4 * q);
-          v[4 * q] = x.x;
-          v[4 * q + 1] = x.y;
-          v[4 * q + 2] = x.z;
-          v[4 * q + 3] = x.w;
-        }
-        image_row32(L, ch, row, v);
-      }
-    }
-    tc::fence_proxy_async();
-    __syncthreads();
-    pc.mark(2);
-    for (int l = 0; l < a.n_attn; ++l) {
-      float* Xl = X + l * a.x_layer_stride;
-      float* Xn = X + (l + 1) * a.x_layer_stride;
-      float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
-      float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * nm4;
-      float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * nm4;
-      const uint8_t* img = a.img_ab[l];
-      // ---- U = X [A|B]: 8 steps (half h = step / 4 -> T0 / T1, K chunk = step % 4)
-      auto issue_copy = [&](int q) {
-        const int hh = q >> 2, kc = q & 3, s = q & 1;
-        const uint8_t* src = img + static_cast<size_t>(kc) * 65536 + hh * 16384;
-        tc::mbar_expect_tx(&L.wb[s], 32768);
-        tc::bulk_g2s(L.ws[s], src, 16384, &L.wb[s]);
-        tc::bulk_g2s(L.ws[s] + 16384, src + 32768, 16384, &L.wb[s]);
-      };
-      if (tid == 0) issue_copy(0);
-      const uint32_t idesc128 = tc::idesc_tf32(128);
-      for (int q = 0; q < 8; ++q) {
-        const int s = q & 1, hh = q >> 2, kc = q & 3;
-        if (tid == 0) {
-          tc::mbar_wait(&L.wb[s], wph[s] & 1u);
-          ++wph[s];
-          tc::fence_after();
-          const uint32_t a0 = tc::smem_u32(L.xi[2 * kc]), a1 = tc::smem_u32(L.xi[2 * kc + 1]);
-          const uint32_t b0 = tc::smem_u32(L.ws[s]), b1 = b0 + 16384;
-          const uint32_t d = hh ? T1 : T0;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t acc = (kc > 0 || kk > 0) ? 1u : 0u;
-            tc::mma_tf32(d, tc::kmajor_sw128_desc(a0 + 32 * kk), tc::kmajor_sw128_desc(b0 + 32 * kk), idesc128, acc);
-            if (NPASS > 1) {
-              tc::mma_tf32(d, tc::kmajor_sw128_desc(a0 + 32 * kk), tc::kmajor_sw128_desc(b1 + 32 * kk), idesc128, 1u);
-              tc::mma_tf32(d, tc::kmajor_sw128_desc(a1 + 32 * kk), tc::kmajor_sw128_desc(b0 + 32 * kk), idesc128, 1u);
-            }
-          }
-          tc::mma_commit(&st.bar[s]);
-        }
-        st.use(s);
-        if (q + 1 < 8) {
-          // the other stage is free once step q-1's MMAs have read it; its copy then
-          // overlaps step q's MMAs
-          tc::wait_stage(st, s ^ 1);
-          if (tid == 0) issue_copy(q + 1);
-        }
-      }
-      mma_wait_all();
-      pc.mark(3);
-      // ---- U_A -> hi (T0) / lo (T2), U stash
-      {
-        float v[32], hi[32], lo[32];
-        for (int cb = 64 * h2; cb < 64 * h2 + 64; cb += 32) {
-          fwd2::tmem_ld32(T0 + lanes + cb, v);
-          if (row < n) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              *reinterpret_cast<float4*>(Ul + row * M2 + cb + 4 * q) =
-                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          }
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            hi[j] = tc::tf32_rn(v[j]);
-            lo[j] = v[j] - hi[j];
-          }
-          fwd2::tmem_st32(T0 + lanes + cb, hi);
-          fwd2::tmem_st32(T2 + lanes + cb, lo);
-          fwd2::tmem_ld32(T1 + lanes + cb, v);
-          if (row < n) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              *reinterpret_cast<float4*>(Ul + row * M2 + M + cb + 4 * q) =
-                  make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          }
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      }
-      tc::fence_before();
-      __syncthreads();
-      pc.mark(4);
-      // ---- S = U_A X^T  (TS; K = 128; N = n rounded to 16)
-      const int NTn = (n + 15) & ~15;
-      if (tid == 0) {
-        tc::fence_after();
-        const uint32_t idesc = tc::idesc_tf32(NTn);
-#pragma unroll 4
-        for (int kk = 0; kk < 16; ++kk) {
-          const int ch = kk >> 2;
-          const uint32_t b0 = tc::smem_u32(L.xi[2 * ch]) + 32 * (kk & 3);
-          const uint32_t b1 = tc::smem_u32(L.xi[2 * ch + 1]) + 32 * (kk & 3);
-          const uint32_t acc = kk > 0 ? 1u : 0u;
-          tc::mma_tf32_ts(T3, T0 + 8 * kk, tc::kmajor_sw128_desc(b0), idesc, acc);
-          if (NPASS > 1) {
-            tc::mma_tf32_ts(T3, T0 + 8 * kk, tc::kmajor_sw128_desc(b1), idesc, 1u);
-            tc::mma_tf32_ts(T3, T2 + 8 * kk, tc::kmajor_sw128_desc(b0), idesc, 1u);
-          }
-        }
-        tc::mma_commit(&st.bar[0]);
-      }
-      st.use(0);
-      mma_wait_all();
-      pc.mark(5);
-      // ---- U_B^T image into XI (the X image is no longer needed): row m, K = j
-      {
-        float v[32];
-        const int ch = row >> 5, kl = row & 31;  // K chunk / position of this thread's j
-        uint8_t* hi = L.xi[2 * ch];
-        uint8_t* lo = L.xi[2 * ch + 1];
-        for (int cb = 64 * h2; cb < 64 * h2 + 64; cb += 32) {
-          fwd2::tmem_ld32(T1 + lanes + cb, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = row < n ? v[j] : 0.f;
-            const float hv = tc::tf32_rn(x);
-            const uint32_t off = tc::sw128_off(cb + j, kl);
-            *reinterpret_cast<float*>(hi + off) = hv;
-            *reinterpret_cast<float*>(lo + off) = x - hv;
-          }
-        }
-      }
-      pc.mark(6);
-      // ---- weighted softmax + gate by rows from TMEM (T3); P~ hi/lo into T0/T2
-      {
-        float sv[64];
-        float* red = L.red;
-        float mx = -FLT_MAX;
-        for (int b = 0; b < 2; ++b) {
-          float v[32];
-          fwd2::tmem_ld32(T3 + lanes + 64 * h2 + 32 * b, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = 64 * h2 + 32 * b + j;
-            sv[32 * b + j] = col < n ? v[j] : -FLT_MAX;
-            mx = fmaxf(mx, sv[32 * b + j]);
-          }
-        }
-        red[h2 * 128 + row] = mx;
-        __syncthreads();
-        mx = fmaxf(red[row], red[128 + row]);
-        __syncthreads();
-        float den = 0.f;
-#pragma unroll
-        for (int j = 0; j < 64; ++j) {
-          const int col = 64 * h2 + j;
-          const float e = col < n ? __expf(sv[j] - mx) : 0.f;
-          sv[j] = e;
-          if (col < n) den += sm.s[col] * sm.s[col] * e;
-        }
-        red[h2 * 128 + row] = den;
-        __syncthreads();
-        den = red[row] + red[128 + row];
-        const float inv = den > 0.f ? 1.0f / den : 0.f;
-        const float4 Rk = row < n ? sm.R[row] : make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int b = 0; b < 2; ++b) {
-          float hi[32], lo[32];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float pu4[4], pt4[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int j = 32 * b + 4 * q + u;
-              const int col = 64 * h2 + j;
-              float pu = 0.f, pt = 0.f;
-              if (row < n && col < n) {
-                const float sj = sm.s[col];
-                pu = sv[j] * inv;
-                pt = sj * sj * pu * (dot4(Rk, sm.R[col]) * inv_sig);
-              }
-              pu4[u] = pu;
-              pt4[u] = pt;
-              hi[4 * q + u] = tc::tf32_rn(pt);
-              lo[4 * q + u] = pt - hi[4 * q + u];
-            }
-            const int col0 = 64 * h2 + 32 * b + 4 * q;
-            if (row < n && col0 < n) {
-              *reinterpret_cast<float4*>(PUl + row * ln + col0) = make_float4(pu4[0], pu4[1], pu4[2], pu4[3]);
-              *reinterpret_cast<float4*>(PTl + row * ln + col0) = make_float4(pt4[0], pt4[1], pt4[2], pt4[3]);
-            }
-          }
-          fwd2::tmem_st32(T0 + lanes + 64 * h2 + 32 * b, hi);
-          fwd2::tmem_st32(T2 + lanes + 64 * h2 + 32 * b, lo);
-        }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      }
-      tc::fence_before();
-      tc::fence_proxy_async();
-      __syncthreads();
-      pc.mark(7);
-      // ---- PV: acc (T1) = P~ U_B  (TS; K = n rounded to 8; N = M)
-      if (tid == 0) {
-        tc::fence_after();
-        const int ksteps = (n + 7) >> 3;
-        for (int kk = 0; kk < ksteps; ++kk) {
-          const int ch = kk >> 2;
-          const uint32_t b0 = tc::smem_u32(L.xi[2 * ch]) + 32 * (kk & 3);
-          const uint32_t b1 = tc::smem_u32(L.xi[2 * ch + 1]) + 32 * (kk & 3);
-          const uint32_t acc = kk > 0 ? 1u : 0u;
-          tc::mma_tf32_ts(T1, T0 + 8 * kk, tc::kmajor_sw128_desc(b0), idesc128, acc);
-          if (NPASS > 1) {
-            tc::mma_tf32_ts(T1, T0 + 8 * kk, tc::kmajor_sw128_desc(b1), idesc128, 1u);
-            tc::mma_tf32_ts(T1, T2 + 8 * kk, tc::kmajor_sw128_desc(b0), idesc128, 1u);
-          }
-        }
-        tc::mma_commit(&st.bar[0]);
-      }
-      st.use(0);
-      mma_wait_all();
-      pc.mark(8);
-      // ---- X' = X + acc: stash, and the X image of the next layer
-      {
-        float v[32];
-        for (int cb = 64 * h2; cb < 64 * h2 + 64; cb += 32) {
-          fwd2::tmem_ld32(T1 + lanes + cb, v);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (row < n) {
-              const float4 xi = *reinterpret_cast<const float4*>(Xl + row * M + cb + 4 * q);
-              x = make_float4(xi.x + v[4 * q], xi.y + v[4 * q + 1], xi.z + v[4 * q + 2], xi.w + v[4 * q + 3]);
-              *reinterpret_cast<float4*>(Xn + row * M + cb + 4 * q) = x;
-            }
-            v[4 * q] = x.x;
-            v[4 * q + 1] = x.y;
-            v[4 * q + 2] = x.z;
-            v[4 * q + 3] = x.w;
-          }
-          __syncthreads();  // every warp has finished reading the U_B^T image (PV done)
-          image_row32(L, cb >> 5, row, v);
-        }
-      }
-      tc::fence_before();
-      tc::fence_proxy_async();
-      __syncthreads();
-      pc.mark(9);
-    }
-    // ---- descriptor from the final X' (image hi + lo == X' exactly)
-    {
-      const int nh = (n + 1) >> 1;
-      const int hf = tid >> 7, m = tid & 127;
-      const int kb = hf * nh, ke = min(n, kb + nh);
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-      const uint8_t* hi = L.xi[2 * (m >> 5)];
-      const uint8_t* lo = L.xi[2 * (m >> 5) + 1];
-      for (int k = kb; k < ke; ++k) {
-        const uint32_t off = tc::sw128_off(k, m & 31);
-        const float x = *reinterpret_cast<const float*>(hi + off) + *reinterpret_cast<const float*>(lo + off);
-        const float4 R = sm.R[k];
-        a0 += x * R.x;
-        a1 += x * R.y;
-        a2 += x * R.z;
-        a3 += x * R.w;
-      }
-      L.part[hf * 128 + m] = make_float4(a0, a1, a2, a3);
-      __syncthreads();
-      if (tid < 128) {
-        const float4 p0 = L.part[tid], p1 = L.part[128 + tid];
-        const float4 A = make_float4((p0.x + p1.x) * a.inv_sqrt_nmax, (p0.y + p1.y) * a.inv_sqrt_nmax,
-                                     (p0.z + p1.z) * a.inv_sqrt_nmax, (p0.w + p1.w) * a.inv_sqrt_nmax);
-        reinterpret_cast<float4*>(sm.Ad)[tid] = A;
-        if (tid < mr) {
-          sm.Bd[0 * mr + tid] = A.x;
-          sm.Bd[1 * mr + tid] = A.y;
-          sm.Bd[2 * mr + tid] = A.z;
-          sm.Bd[3 * mr + tid] = A.w;
-        }
-      }
-      __syncthreads();
-      float* D = a.D + static_cast<size_t>(c) * M * mr;
-      for (int idx = tid; idx < M * mr; idx += blockDim.x) {
-        const int mm_ = idx / mr, q = idx - mm_ * mr;
-        float acc = 0.f;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) acc += sm.Ad[mm_ * 4 + cc] * sm.Bd[cc * mr + q];
-        D[idx] = acc;
-      }
-      for (int idx = tid; idx < M * 4; idx += blockDim.x) a.Ad[static_cast<size_t>(c) * M * 4 + idx] = sm.Ad[idx];
-      for (int idx = tid; idx < 4 * mr; idx += blockDim.x) a.Bd[static_cast<size_t>(c) * 4 * mr + idx] = sm.Bd[idx];
-      tc::fence_proxy_async();
-      __syncthreads();
-      pc.mark(10);
-    }
-  }
-  pc.flush();
-  mm.finish();
-}
-
-size_t forward2_smem_bytes(const DpArgs& a) {
-  return 1024 + fwd2::kHead + 6 * 16384 + 64 + 1024 + 4096 + sizeof(float4) * a.n_max +
-         2 * (((sizeof(float) * a.n_max + 15) / 16) * 16) + sizeof(float) * a.M * 4 + 16 * ((4 * a.mr * 4 + 15) / 16) +
-         sizeof(double) * 32 + 64;
-}
-
-// ------------------------------------------------------------------------------------
 // Backward: dD -> (dA, dB) -> dX, dR -> attention layers in reverse -> embedding ->
 // row gradients g_k = de/dd_k (FP64 geometry), per-centre virial -sum g (x) d.
 // ------------------------------------------------------------------------------------
@@ -1583,26 +1131,10 @@ static void set_smem(size_t smem) {
   ensure_smem_attr(reinterpret_cast<const void*>(k_centre_backward<MODE, WIMG>), smem);
 }
 
-// a.wimg: every weight GEMM has a pre-split image (tensor-core modes) -> the WIMG kernels
-template <int NPASS>
-static void launch_forward2(const DpArgs& a, int n_sm, cudaStream_t st) {
-  const size_t smem = forward2_smem_bytes(a);
-  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_forward2<NPASS, true>), smem);
-  k_centre_forward2<NPASS, true><<<n_sm, 256, smem, st>>>(a);
-  count_launch();
-}
-
 template <bool FWD>
 static void launch_centre(const DpArgs& a, int grid, cudaStream_t st) {
   if (a.n_centres == 0) return;
   cudaMemsetAsync(a.work, 0, sizeof(int), st);
-  if (FWD && a.fwd2 && a.mode != 0) {
-    // one CTA per SM (grid = 2 CTAs per SM for the other kernels)
-    const int n_sm = (grid + 1) / 2;
-    if (a.mode == 1) launch_forward2<3>(a, n_sm, st);
-    else launch_forward2<1>(a, n_sm, st);
-    return;
-  }
   const size_t smem = dp_smem_bytes(a, a.mode);
   auto go = [&](auto mode_c, auto wimg_c) {
     constexpr int MODE = decltype(mode_c)::value;

@@ -188,10 +188,8 @@ struct DpArgs {
   const uint8_t* img_ew[kMaxLayers];
   const uint8_t* img_ewT[kMaxLayers];
   int wimg;  // 1: all of the above are present (the per-centre kernels' WIMG variant)
-  int fwd2;  // 1: the on-chip chained forward (k_centre_forward2): wimg, M == 128, n <= 128
   int* work;  // dynamic centre counter of the persistent per-centre kernels (zeroed per launch)
 };
-size_t forward2_smem_bytes(const DpArgs& a);
 // Weight images: bytes for a K x N operand, and the builder (B(k,n) = TB ? W[n*ldb+k] :
 // W[k*ldb+n]).
 size_t weight_image_bytes(int K, int N);

@@ -276,22 +276,3 @@ def test_paper_model_cutoff_sweep_spotcheck(rc):
         assert abs(r1["atom_energy"][c] - e) <= 1e-5 * max(abs(e), 1e-2), (c, r1["atom_energy"][c], e)
     port.model_free(h)
 
-
-def test_chained_forward_experimental_path(monkeypatch):
-    """k_centre_forward2 (on-chip chained attention layers, opt-in NNMD_FWD2=1) against the
-    default two-CTA forward on the paper model: same rows, energies within 1e-5."""
-    import subprocess
-    import sys
-    import os
-    code = ("import numpy as np, paper_2604_07276_b200 as nb\n"
-            "box, pos, sp = nb.synth_system(1500, 0.1, 0.9, 4)\n"
-            "m = nb.init_model(nb.paper_spec(6.0), 1)\n"
-            "r = nb.DeviceEvaluator(m, n_ranks=1).compute(pos, sp, box)\n"
-            "np.save('/tmp/fwd2_%s.npy', np.concatenate([[r['energy']], r['forces'].ravel(), r['atom_energy']]))\n")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for tag, env in (("ref", {}), ("fwd2", {"NNMD_FWD2": "1"})):
-        subprocess.run([sys.executable, "-c", code % tag], check=True, cwd=root, env={**os.environ, **env})
-    a, b = np.load("/tmp/fwd2_ref.npy"), np.load("/tmp/fwd2_fwd2.npy")
-    assert abs(a[0] - b[0]) <= 1e-5 * abs(a[0])
-    n = (len(a) - 1) // 4
-    assert rel_err(b[1:1 + 3 * n], a[1:1 + 3 * n]) <= 1e-5
