@@ -81,6 +81,21 @@ nnmd_status nnmd_model_set_n_max(nnmd_model* m, int n_max);
 /* partition_ranks (decomp.cpp:17-57): surface-minimising p_x*p_y*p_z = n_ranks. */
 nnmd_status nnmd_partition_ranks(const double box[3], int n_ranks, double min_edge, int dims[3]);
 
+/* Ghost-force route plan of one process (decomp.cpp:445-469; DD rank r runs in process
+ * r % world_size): counts[s*n_ranks + o] = routed entries from source rank s to owner rank o.
+ * Writes up to cap ops {kind 0 send / 1 receive, src, dst, peer process, offset (entries
+ * into the source's send buffer, grouped by every destination, or into its receive buffer,
+ * grouped by this process's destinations), count}; returns the op count (< 0: error).
+ * Sends and receives are in (source, destination) order on every process, so transfers
+ * between one pair of processes match in posting order (ncclSend/ncclRecv in one group). */
+typedef struct {
+  int kind, src, dst, peer;
+  long offset;
+  int count;
+} nnmd_route_op;
+int nnmd_route_schedule(int n_ranks, int world_size, int world_rank, const int* counts, nnmd_route_op* out,
+                        int cap);
+
 /* ---- device context ----------------------------------------------------------------- */
 nnmd_status nnmd_b200_create(const nnmd_model* m, const nnmd_b200_opts* opts, nnmd_b200** out);
 void nnmd_b200_destroy(nnmd_b200* ctx);
@@ -98,10 +113,13 @@ nnmd_status nnmd_b200_compute(nnmd_b200* ctx, int64_t n, const double* coords,
                               double* virial, double* atom_energy);
 
 /* Same evaluation on DEVICE-resident inputs/outputs (pointers on ctx's device); no bulk
- * host copies.  Host synchronisation points per call: one per DD rank handled by this
- * process (the locals/ghosts count read-back that sizes the rank's buffers; wide_halo adds
- * a second for the centre count) and one at the end (step flags: overflow / wrap errors
- * and route counts, all-reduced over processes so that every process throws together).
+ * host copies.  Host synchronisation points per call (cudaStreamSynchronize):
+ *   - one per DD rank handled by this process: the locals/ghosts count read-back that
+ *     sizes the rank's buffers (wide_halo adds a second, for the centre count);
+ *   - with world_size > 1 and masked_reduction, one after the all-reduce of the route
+ *     counts, which sizes the point-to-point ghost-force transfers;
+ *   - one at the end: step flags (overflow / wrap errors and route counts, all-reduced over
+ *     processes so that every process throws together) and the per-kernel event times.
  * The call returns with the stream idle.  With world_size > 1 the positions of world
  * rank 0 are broadcast to all processes (collective 1) before the DD build.
  * d_out layout (float64): [energy, virial(9), forces(3n), atom_energy(n)]. */

@@ -122,6 +122,8 @@ def lib():
     L.nnmd_model_get_spec.argtypes = [C.c_void_p, C.POINTER(_Spec)]
     L.nnmd_model_set_n_max.argtypes = [C.c_void_p, C.c_int]
     L.nnmd_partition_ranks.argtypes = [_dp, C.c_int, C.c_double, _ip]
+    L.nnmd_route_schedule.argtypes = [C.c_int, C.c_int, C.c_int, _ip, C.c_void_p, C.c_int]
+    L.nnmd_route_schedule.restype = C.c_int
     L.nnmd_b200_create.argtypes = [C.c_void_p, C.POINTER(_Opts), C.POINTER(C.c_void_p)]
     L.nnmd_b200_destroy.argtypes = [C.c_void_p]
     L.nnmd_b200_nccl_unique_id.argtypes = [C.c_void_p]
@@ -259,6 +261,26 @@ def partition_ranks(box, n_ranks: int, min_edge: float = 0.0) -> np.ndarray:
     _check(lib().nnmd_partition_ranks(_d(np.asarray(box, dtype=np.float64)), n_ranks, min_edge,
                                       dims.ctypes.data_as(_ip)))
     return dims
+
+
+class _RouteOp(C.Structure):
+    _fields_ = [("kind", C.c_int), ("src", C.c_int), ("dst", C.c_int), ("peer", C.c_int),
+                ("offset", C.c_long), ("count", C.c_int)]
+
+
+def route_schedule(n_ranks: int, world_size: int, world_rank: int, counts) -> list:
+    """Point-to-point plan of the ghost-force route for one process (host only; the plan
+    the device path posts as one ncclGroupStart/End of ncclSend/ncclRecv).  counts[s, o] =
+    routed entries from DD rank s to owner rank o.  Returns dicts {kind: "send"|"recv",
+    src, dst, peer, offset, count} in posting order."""
+    cnt = np.ascontiguousarray(np.asarray(counts, dtype=np.int32).reshape(n_ranks, n_ranks))
+    cap = n_ranks * n_ranks
+    ops = (_RouteOp * max(cap, 1))()
+    k = lib().nnmd_route_schedule(n_ranks, world_size, world_rank, cnt.ctypes.data_as(_ip), ops, cap)
+    if k < 0:
+        raise Error(lib().nnmd_b200_last_error().decode())
+    return [dict(kind="send" if o.kind == 0 else "recv", src=o.src, dst=o.dst, peer=o.peer, offset=o.offset,
+                 count=o.count) for o in ops[:k]]
 
 
 def synth_system(n: int, rho: float = 0.1, min_sep: float = 0.9, seed: int = 1):

@@ -121,6 +121,19 @@ nnmd_status nnmd_partition_ranks(const double box[3], int n_ranks, double min_ed
   });
 }
 
+int nnmd_route_schedule(int n_ranks, int world_size, int world_rank, const int* counts, nnmd_route_op* out,
+                        int cap) {
+  int n = -1;
+  const nnmd_status st = guarded([&] {
+    const auto ops = nb::route_schedule(n_ranks, world_size, world_rank, counts);
+    nb::require(out || ops.empty() || cap == 0, "nnmd_route_schedule: null output");
+    for (size_t i = 0; i < ops.size() && static_cast<int>(i) < cap; ++i)
+      out[i] = {ops[i].kind, ops[i].src, ops[i].dst, ops[i].peer, ops[i].offset, ops[i].count};
+    n = static_cast<int>(ops.size());
+  });
+  return st == NNMD_OK ? n : -1;
+}
+
 nnmd_status nnmd_b200_create(const nnmd_model* m, const nnmd_b200_opts* opts, nnmd_b200** out) {
   return guarded([&] {
     nb::require(m && opts && out, "nnmd_b200_create: null argument");

@@ -120,6 +120,7 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   build_weight_images();
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_counts_), 64 * sizeof(int)));
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_flags_), (kFlagWords + 64) * sizeof(int)));
+  CU(cudaMallocHost(reinterpret_cast<void**>(&h_rcnt_), kMaxRanks * kMaxRanks * sizeof(int)));
   require(o.n_ranks <= 48, "nnmd_b200: at most 48 DD ranks");
   stats_.resize(static_cast<size_t>(o.n_ranks));
   debug_.resize(static_cast<size_t>(o.n_ranks));
@@ -150,6 +151,7 @@ Context::~Context() {
     if (e) cudaEventDestroy(e);
   if (h_counts_) cudaFreeHost(h_counts_);
   if (h_flags_) cudaFreeHost(h_flags_);
+  if (h_rcnt_) cudaFreeHost(h_rcnt_);
   if (h_out_) cudaFreeHost(h_out_);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -209,8 +211,15 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   phases_.clear();
   pool_used_ = 0;
   for (auto& s : stats_) s = RankStat{};
-  const size_t out_len = 10 + 4 * static_cast<size_t>(n);
-  CU(cudaMemsetAsync(d_out, 0, out_len * sizeof(double), st_));
+  const int R = opts_.n_ranks;
+  // step result: per-rank [E, W] rows, forces and atom energies of the owned atoms (each
+  // element has exactly one writer, so the cross-process sum is exact)
+  red_.ensure(10 * static_cast<size_t>(R) + 4 * static_cast<size_t>(n) + 1);
+  CU(cudaMemsetAsync(red_.p, 0, (10 * static_cast<size_t>(R) + 4 * static_cast<size_t>(n)) * sizeof(double), st_));
+  fown_.ensure(3 * static_cast<size_t>(n) + 3);
+  rcnt_.ensure(2 * static_cast<size_t>(R) * R);
+  CU(cudaMemsetAsync(rcnt_.p, 0, 2 * static_cast<size_t>(R) * R * sizeof(int), st_));
+  route_cap_ = 0;
   owner_.ensure(static_cast<size_t>(n) + 1);
   err_.ensure(8);
   CU(cudaMemsetAsync(err_.p, 0x7f, 8 * sizeof(int), st_));
@@ -243,19 +252,9 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   flags_.ensure(kFlagWords + opts_.n_ranks);
   CU(cudaMemsetAsync(flags_.p, 0, (kFlagWords + opts_.n_ranks) * sizeof(int), st_));
   for (int r = 0; r < opts_.n_ranks; ++r)
-    if (r % opts_.world_size == opts_.world_rank) run_rank(r, sys, dims.data(), thickness, d_out, keep_debug_);
+    if (r % opts_.world_size == opts_.world_rank) run_rank(r, sys, dims.data(), thickness, keep_debug_);
   launch_negate(err_.p, flags_.p, kFlagWords, st_);
-  if (use_nccl_) {
-    // collective 2 (reduce_forces, decomp.cpp:188-204, 471-538): [E, W, F, e_i] summed
-    // over processes; then the error words and route counts, so that every process sees
-    // an overflow on any rank and all of them throw together
-    tic("nccl_allreduce");
-    const Nccl& N = nccl();
-    int rc = N.AllReduce(d_out, d_out, out_len, kNcclFloat64, kNcclSum, comm_, st_);
-    if (rc == 0) rc = N.AllReduce(flags_.p, flags_.p, kFlagWords + opts_.n_ranks, kNcclInt32, kNcclMax, comm_, st_);
-    if (rc != 0) throw CudaError(std::string("ncclAllReduce: ") + N.GetErrorString(rc));
-    toc();
-  }
+  route_and_reduce(n, d_out);
   CU(cudaMemcpyAsync(h_flags_, flags_.p, (kFlagWords + opts_.n_ranks) * sizeof(int), cudaMemcpyDeviceToHost, st_));
   CU(cudaStreamSynchronize(st_));
   collect_times();
@@ -285,8 +284,108 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   }
 }
 
+std::vector<RouteOp> route_schedule(int R, int ws, int wr, const int* counts) {
+  require(R >= 1 && R <= kMaxRanks && ws >= 1 && wr >= 0 && wr < ws && counts, "route_schedule: bad argument");
+  auto local = [&](int r) { return r % ws == wr; };
+  std::vector<RouteOp> ops;
+  for (int s = 0; s < R; ++s) {
+    long soff = 0, roff = 0;
+    for (int o = 0; o < R; ++o) {
+      const int c = counts[s * R + o];
+      require(c >= 0, "route_schedule: negative count");
+      if (c > 0 && local(s) && !local(o)) ops.push_back({0, s, o, o % ws, soff, c});
+      if (c > 0 && !local(s) && local(o)) ops.push_back({1, s, o, s % ws, roff, c});
+      soff += c;
+      if (local(o)) roff += c;
+    }
+  }
+  return ops;
+}
+
+// Ghost-force route and reduce_forces (decomp.cpp:445-538).  Every DD rank has packed the
+// owner's zero-image partials of its locals (fown, e_i) and its routed ghost partials,
+// grouped by owner rank (run_rank).  With several processes the (source, destination)
+// entry counts are all-reduced and the entries move point to point (ncclSend/ncclRecv,
+// one grouped call; only pairs with entries).  Each process then merges, for the atoms its
+// ranks own: zero-image partial first, then routed partials in (zero image first, image,
+// rank) order -- the reference's merge order, and independent of arrival order.  Every
+// element of the result [rows | F | e_i] has exactly one writer, so the final all-reduce
+// is exact; the per-rank [E, W] rows are summed in rank order (launch_finalize).
+void Context::route_and_reduce(long n, double* d_out) {
+  const int R = opts_.n_ranks, ws = opts_.world_size, wr = opts_.world_rank;
+  const bool masked = opts_.scheme == NNMD_MASKED_REDUCTION;
+  const bool multi = use_nccl_ && ws > 1;
+  MergeArgs ma{};
+  ma.n_ranks = R;
+  ma.world_size = ws;
+  ma.world_rank = wr;
+  ma.n_atoms = static_cast<int>(n);
+  ma.cnt = rcnt_.p;
+  long capacity = route_cap_;
+  for (int s = 0; s < R; ++s) ma.src_base[s] = route_buf_[s].p;
+  if (multi && masked) {
+    tic("nccl_route");
+    const Nccl& N = nccl();
+    int rc = N.AllReduce(rcnt_.p, rcnt_.p, static_cast<size_t>(R) * R, kNcclInt32, kNcclSum, comm_, st_);
+    if (rc != 0) throw CudaError(std::string("ncclAllReduce (route counts): ") + N.GetErrorString(rc));
+    CU(cudaMemcpyAsync(h_rcnt_, rcnt_.p, static_cast<size_t>(R) * R * sizeof(int), cudaMemcpyDeviceToHost, st_));
+    CU(cudaStreamSynchronize(st_));
+    auto local = [&](int r) { return r % ws == wr; };
+    for (int s = 0; s < R; ++s) {
+      if (local(s)) continue;
+      long tot = 0;
+      for (int o = 0; o < R; ++o)
+        if (local(o)) tot += h_rcnt_[s * R + o];
+      recv_buf_[s].ensure(static_cast<size_t>(tot) + 1);
+      ma.src_base[s] = recv_buf_[s].p;
+      capacity += tot;
+    }
+    rc = N.GroupStart();
+    for (const RouteOp& op : route_schedule(R, ws, wr, h_rcnt_)) {
+      if (rc != 0) break;
+      const size_t bytes = static_cast<size_t>(op.count) * sizeof(RouteEntry);
+      if (op.kind == 0) rc = N.Send(route_buf_[op.src].p + op.offset, bytes, kNcclUint8, op.peer, comm_, st_);
+      else rc = N.Recv(recv_buf_[op.src].p + op.offset, bytes, kNcclUint8, op.peer, comm_, st_);
+    }
+    const int rc2 = N.GroupEnd();
+    if (rc == 0) rc = rc2;
+    if (rc != 0) throw CudaError(std::string("ncclSend/ncclRecv (ghost-force route): ") + N.GetErrorString(rc));
+    toc();
+  }
+  inc_cnt_.ensure(static_cast<size_t>(n) + 1);
+  inc_off_.ensure(static_cast<size_t>(n) + 1);
+  seg_.ensure(2 * static_cast<size_t>(R) * R + 1);
+  inc_.ensure(static_cast<size_t>(capacity) + 1);
+  CU(cudaMemsetAsync(inc_cnt_.p, 0, (static_cast<size_t>(n) + 1) * sizeof(int), st_));
+  ma.seg = seg_.p;
+  ma.inc_cnt = inc_cnt_.p;
+  ma.inc_off = inc_off_.p;
+  ma.inc = inc_.p;
+  ma.capacity = static_cast<int>(capacity);
+  ma.owner = owner_.p;
+  ma.fown = fown_.p;
+  ma.f_out = red_.p + 10 * static_cast<size_t>(R);
+  tic("route_merge");
+  launch_route_merge(ma, st_);
+  toc();
+  if (use_nccl_) {
+    // collective 2 (reduce_forces, decomp.cpp:188-204): the result rows, forces and atom
+    // energies summed over processes (one writer per element: exact); then the error
+    // words and route counts, so that every process sees an overflow on any rank and all
+    // of them throw together
+    tic("nccl_allreduce");
+    const Nccl& N = nccl();
+    const size_t len = 10 * static_cast<size_t>(R) + 4 * static_cast<size_t>(n);
+    int rc = N.AllReduce(red_.p, red_.p, len, kNcclFloat64, kNcclSum, comm_, st_);
+    if (rc == 0) rc = N.AllReduce(flags_.p, flags_.p, kFlagWords + R, kNcclInt32, kNcclMax, comm_, st_);
+    if (rc != 0) throw CudaError(std::string("ncclAllReduce: ") + N.GetErrorString(rc));
+    toc();
+  }
+  launch_finalize(red_.p, R, n, d_out, st_);
+}
+
 void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double thickness,
-                       double* d_out, bool keep_debug) {
+                       bool keep_debug) {
   const Model& m = model_;
   const int n = sys.n;
   const bool wide = opts_.scheme == NNMD_WIDE_HALO;
@@ -420,6 +519,14 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   na.cs = csd;
   na.n_max = nmax;
   na.rc2 = m.rc * m.rc;
+  {
+    // sort keys pack (species, bits(r2)) into 64 bits: r2 < rc2 has an exponent field <=
+    // that of rc2, so 6 exponent bits (2^-63 of rc2 and up) plus the 52 mantissa bits fit
+    uint64_t rb;
+    std::memcpy(&rb, &na.rc2, sizeof rb);
+    const uint64_t emax = rb >> 52;
+    na.kbase = emax >= 63 ? (emax - 63) << 52 : 0;
+  }
   na.centre_member = cen_member_.p;
   na.n_lists = ncen;
   na.cand_limit = INT_MAX;
@@ -430,6 +537,15 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   maxn_.ensure(1);
   CU(cudaMemsetAsync(maxn_.p, 0, sizeof(int), st_));
   na.maxn = maxn_.p;
+  // environment matrix fused into the centre-list build (k_neighbors writes R, Z, sigma)
+  R_.ensure(static_cast<size_t>(ncen) * nmax + 1);
+  Z_.ensure(static_cast<size_t>(ncen) * nmax + 1);
+  sig_.ensure(ncen + 1);
+  na.R = R_.p;
+  na.Z = Z_.p;
+  na.sig = sig_.p;
+  na.rc = m.rc;
+  na.rcs = m.rcs;
   tic("neighbors");
   launch_neighbors(na, st_);
   toc();
@@ -446,6 +562,9 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     rv.nn = rn_.p;
     rv.err = err_.p + 2;
     rv.nonempty = counts_.p + 3;
+    rv.R = nullptr;  // reverse lists carry no env rows
+    rv.Z = nullptr;
+    rv.sig = nullptr;
     tic("neighbors_reverse");
     launch_neighbors(rv, st_);
     toc();
@@ -491,7 +610,6 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.nn = nn_.p;
   dp.x_layer_stride = static_cast<size_t>(ncen) * nmax * M;
   X_.ensure(dp.x_layer_stride * (m.na + 1) + 4);
-  R_.ensure(static_cast<size_t>(ncen) * nmax + 1);
   Ad_.ensure(static_cast<size_t>(ncen) * M * 4 + 4);
   Bd_.ensure(static_cast<size_t>(ncen) * 4 * mr + 4);
   D_.ensure(static_cast<size_t>(ncen) * M * mr + 4);
@@ -515,8 +633,6 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     dp.PTst = PTst_.p;
     dp.EMBst = EMBst_.p;
   }
-  Z_.ensure(static_cast<size_t>(ncen) * nmax + 1);
-  sig_.ensure(ncen + 1);
   dp.Z = Z_.p;
   dp.sig = sig_.p;
   dp.X = X_.p;
@@ -558,9 +674,6 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     CU(cudaMemsetAsync(fbuf.p, 0, 24 * sizeof(unsigned long long), st_));
     dp.prof = fbuf.p;
   }
-  tic("env");
-  launch_env(dp, st_);
-  toc();
   tic("centre_forward");
   launch_centre_forward(dp, grid, st_);
   toc();
@@ -654,20 +767,31 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   tic("force_gather");
   launch_force_gather(fo, st_);
   toc();
-  AssembleArgs as{};
-  as.n_atoms = n;
-  as.rank = rank;
-  as.wide = wide;
-  as.owner = owner_.p;
-  as.loc_off = loc_off_.p;
-  as.gh_off = gh_off_.p;
-  as.counts = counts_.p;
-  as.fmem = fmem_.p;
-  as.e_centre = e_.p;
-  as.out = d_out;
-  tic("assemble");
-  launch_assemble(as, st_);
-  launch_energy_virial(e_.p, vir_.p, counts_.p, d_out, st_);
+  // ghost-force route, pack side: the owner's zero-image partials of the locals, the routed
+  // ghost partials grouped by owner rank (decomp.cpp:445-455); this rank's [E, W] row
+  if (!wide) route_buf_[rank].ensure(static_cast<size_t>(ngh) + 1);
+  RouteArgs ro{};
+  ro.rank = rank;
+  ro.n_ranks = opts_.n_ranks;
+  ro.wide = wide;
+  ro.nloc = nloc;
+  ro.ngh = ngh;
+  ro.m_atom = m_atom_.p;
+  ro.m_shift = m_shift_.p;
+  ro.m_owner = m_owner_.p;
+  ro.rn = wide ? nullptr : rn_.p;
+  ro.fmem = fmem_.p;
+  ro.e_centre = e_.p;
+  ro.fown = fown_.p;
+  ro.eown = red_.p + 10 * static_cast<size_t>(opts_.n_ranks) + 3 * static_cast<size_t>(n);
+  ro.cnt = rcnt_.p;
+  ro.cur = rcnt_.p + static_cast<size_t>(opts_.n_ranks) * opts_.n_ranks + static_cast<size_t>(rank) * opts_.n_ranks;
+  ro.buf = wide ? nullptr : route_buf_[rank].p;
+  if (!wide) route_cap_ += ngh;
+  tic("route_pack");
+  launch_route_pack(ro, st_);
+  evpart_.ensure(kEnergyVirialPartials);
+  launch_energy_virial(e_.p, vir_.p, counts_.p, evpart_.p, red_.p + 10 * static_cast<size_t>(rank), st_);
   toc();
   phases_.push_back({rank, 3, ph_f0, timers_.size() - 1});
   if (!wide)
@@ -821,8 +945,10 @@ void Context::record_trace(long n, const std::vector<int>& local_ranks) {
   if (trace_on_) {
     const Timer* owner = nullptr;
     const Timer* nccl = nullptr;
+    const Timer* merge = nullptr;
     for (const auto& t : timers_) {
       if (t.name == "owner") owner = &t;
+      if (t.name == "route_merge") merge = &t;
       if (t.name == "nccl_allreduce") nccl = &t;
       if (t.name == "nccl_broadcast") owner = &t;  // collective 1 proper when there is one
     }
@@ -837,6 +963,7 @@ void Context::record_trace(long n, const std::vector<int>& local_ranks) {
         f1 = std::max(f1, t1);
       }
     }
+    if (merge) f1 = std::max(f1, ev_time(merge->b));
     if (f1 >= f0) {
       if (masked) spans_.push_back({-1, 5, f0, f1, step_});
       if (nccl) spans_.push_back({-1, 6, ev_time(nccl->a), ev_time(nccl->b), step_});

@@ -106,8 +106,7 @@ class Context {
   std::vector<std::pair<std::string, double>> kernel_times() const { return ktimes_; }
 
  private:
-  void run_rank(int rank, const SysArgs& sys, const int dims[3], double thickness, double* d_out,
-                bool keep_debug);
+  void run_rank(int rank, const SysArgs& sys, const int dims[3], double thickness, bool keep_debug);
   bool bcast_positions() const { return use_nccl_; }
   bool coords_needed() const { return !bcast_positions() || opts_.world_rank == 0; }
   static constexpr int kFlagWords = 8;
@@ -154,6 +153,18 @@ class Context {
   DevBuf<float4> R_;
   DevBuf<double> g_, vir_, e_, fmem_, sig_;
   DevBuf<int> Z_;
+  // ghost-force route and the step result (decomp.cpp:445-538)
+  DevBuf<double> red_;    // [R][10] per-rank [E, W9] rows | F [n][3] | e_i [n]  (reduced)
+  DevBuf<double> fown_;   // [n][3] owner's zero-image partial
+  DevBuf<double> evpart_;  // energy/virial block partials
+  DevBuf<int> rcnt_;      // [R][R] routed entries src -> dst, then [R][R] fill cursors
+  DevBuf<RouteEntry> route_buf_[kMaxRanks];  // per local source rank, grouped by destination
+  DevBuf<RouteEntry> recv_buf_[kMaxRanks];   // per remote source rank (world_size > 1)
+  DevBuf<int> inc_cnt_, inc_off_, seg_;
+  DevBuf<const RouteEntry*> inc_;
+  long route_cap_ = 0;       // entries in the local send buffers this step
+  int* h_rcnt_ = nullptr;    // pinned [R][R]
+  void route_and_reduce(long n, double* d_out);
   int* h_counts_ = nullptr;  // pinned
   std::vector<RankStat> stats_;
   std::vector<RankDebug> debug_;
@@ -187,6 +198,20 @@ class Context {
 };
 
 std::vector<int> partition_ranks(const double L[3], int n_ranks, double min_edge);
+
+// Point-to-point plan of the ghost-force route for one process (DD rank r lives in process
+// r % world_size): counts[s * R + o] routed entries from source rank s to owner rank o.
+// Sends and receives are listed in (source, destination) order on every process, so the
+// several transfers between one pair of processes match in posting order.  offset: entries
+// into the source's send buffer (grouped by every destination) for a send, into the
+// source's receive buffer (grouped by this process's destinations) for a receive.
+struct RouteOp {
+  int kind;  // 0 send, 1 receive
+  int src, dst, peer;
+  long offset;
+  int count;
+};
+std::vector<RouteOp> route_schedule(int n_ranks, int world_size, int world_rank, const int* counts);
 
 }  // namespace nb
 

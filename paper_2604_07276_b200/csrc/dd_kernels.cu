@@ -7,6 +7,9 @@
 #include <atomic>
 #include <climits>
 
+#include <algorithm>
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -282,8 +285,13 @@ constexpr int kNbrWarps = 4;
 struct NbrEntry {
   double r2;
   int64_t gid;
+  uint64_t key;  // (species << 58) | (bits(r2) - kbase): same order as (species, r2)
   int member;
   int species;
+};
+// centre lists also keep the image delta centre -> neighbour for their env rows
+struct NbrEntryEnv : NbrEntry {
+  double d[3];
 };
 
 __device__ __forceinline__ bool key_less(const NbrEntry& a, const NbrEntry& b) {
@@ -292,10 +300,43 @@ __device__ __forceinline__ bool key_less(const NbrEntry& a, const NbrEntry& b) {
   return a.gid < b.gid;
 }
 
+// Environment matrix of one canonical row (prepare_rows + switch_eval, dp_core.hpp:116-137,
+// 200-223), fused into the centre-list build: r and s(r) in exact FP64 from the image
+// delta the distance test already formed, env row R = (s, s/r d) as one 16-byte store,
+// the neighbour's species; returns s^2 for sigma.
+__device__ __forceinline__ double env_row(const NbrArgs& a, int li, int k, const NbrEntryEnv& e) {
+  const double r = sqrt(e.r2);
+  double sw, ds;
+  switch_fn(r, a.rcs, a.rc, sw, ds);
+  const double sr = sw / r;
+  const size_t o = static_cast<size_t>(li) * a.n_max + k;
+  a.R[o] = make_float4(static_cast<float>(sw), static_cast<float>(sr * e.d[0]), static_cast<float>(sr * e.d[1]),
+                       static_cast<float>(sr * e.d[2]));
+  a.Z[o] = e.species;
+  return sw * sw;
+}
+
+// Rows of one list (each lane its entries lane, lane + 32, ... at ranks rank[]), then
+// sigma = sum_k s_k^2 (FP64, lane partials in a fixed order, then a fixed warp tree).
+template <int P>
+__device__ __forceinline__ void env_rows(const NbrArgs& a, int li, int cnt, const int (&rank)[P],
+                                         const NbrEntryEnv* buf) {
+  const int lane = threadIdx.x & 31;
+  double sig = 0.0;
+#pragma unroll
+  for (int u = 0; u < P; ++u)
+    if (lane + 32 * u < cnt) sig += env_row(a, li, rank[u], buf[lane + 32 * u]);
+  sig = warp_sum(sig);
+  if (lane == 0) a.sig[li] = sig;
+}
+
+// ENV: centre lists, which also write their environment rows (env_row).
+template <bool ENV>
 __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap) {
-  extern __shared__ NbrEntry nbr_smem[];
+  using Entry = typename std::conditional<ENV, NbrEntryEnv, NbrEntry>::type;
+  extern __shared__ __align__(16) unsigned char nbr_smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  NbrEntry* buf = nbr_smem + static_cast<size_t>(wid) * cap;
+  Entry* buf = reinterpret_cast<Entry*>(nbr_smem_raw) + static_cast<size_t>(wid) * cap;
   const int li = blockIdx.x * kNbrWarps + wid;
   if (li >= a.n_lists) return;
   const int cm = a.centre_member ? a.centre_member[li] : li + a.member_offset;
@@ -307,6 +348,7 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
   const int cz = cell % a.cdims[2], cy = (cell / a.cdims[2]) % a.cdims[1],
             cx = cell / (a.cdims[1] * a.cdims[2]);
   int cnt = 0;
+  bool packable = true;  // every kept key fits the 64-bit packing (per lane)
   for (int ox = -1; ox <= 1; ++ox) {
     const int x = cx + ox;
     if (x < 0 || x >= a.cdims[0]) continue;
@@ -321,7 +363,7 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
         for (int base = b; base < e; base += 32) {
           const int j = base + lane;
           bool keep = false;
-          NbrEntry ent;
+          Entry ent;
           if (j < e) {
             const int mj = a.cell_members[j];
             if (mj != cm && mj < a.cand_limit) {
@@ -337,6 +379,15 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
                 ent.gid = a.cs.gid[j];
                 ent.member = mj;
                 ent.species = a.cs.species[j];
+                if constexpr (ENV) {
+                  ent.d[0] = dx;
+                  ent.d[1] = dy;
+                  ent.d[2] = dz;
+                }
+                const uint64_t rb = static_cast<uint64_t>(__double_as_longlong(r2));
+                const bool ok = rb >= a.kbase && ent.species >= 0 && ent.species < 63;
+                packable = packable && ok;
+                ent.key = (static_cast<uint64_t>(ent.species) << 58) | (rb - a.kbase);
               }
             }
           }
@@ -362,33 +413,64 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
   }
   // rank sort on the unique key: each lane ranks its (up to kPer) entries against one
   // broadcast read of every entry, so the shared-memory sweep is done once per warp
-  // instead of once per entry
+  // instead of once per entry.  Fast path: one 64-bit compare of the packed (species, r2)
+  // key per pair; a list with equal keys (an exact r2 tie within a species) or a key that
+  // does not pack takes the full (species, r2, gid) comparison.
   int* out = a.nlist + static_cast<size_t>(li) * a.n_max;
   constexpr int kPer = 6;  // lanes own entries lane, lane + 32, ... (n_max <= 192)
   if (cnt <= 32 * kPer) {
-    NbrEntry mine[kPer];
+    uint64_t mine[kPer];
     int rank[kPer];
+    const int nu = (cnt + 31) >> 5;  // warp-uniform
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       rank[u] = 0;
-      if (lane + 32 * u < cnt) mine[u] = buf[lane + 32 * u];
+      mine[u] = lane + 32 * u < cnt ? buf[lane + 32 * u].key : ~0ull;
     }
-    const int nu = (cnt + 31) >> 5;  // warp-uniform
-    for (int j = 0; j < cnt; ++j) {
-      const NbrEntry o = buf[j];
+    bool fast = __all_sync(0xffffffffu, packable);
+    if (fast) {
+      int eq = 0;
+      const uint64_t* kb = &buf[0].key;
+      for (int j = 0; j < cnt; ++j) {
+        const uint64_t o = kb[j * (sizeof(Entry) / sizeof(uint64_t))];
 #pragma unroll
-      for (int u = 0; u < kPer; ++u)
-        if (u < nu) rank[u] += key_less(o, mine[u]);
+        for (int u = 0; u < kPer; ++u)
+          if (u < nu) {
+            rank[u] += o < mine[u];
+            eq += o == mine[u];
+          }
+      }
+      // each valid entry meets itself once; padding keys (~0) never equal a packed key
+      int own = 0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) own += (lane + 32 * u < cnt);
+      fast = __all_sync(0xffffffffu, eq == own);
+    }
+    if (!fast) {
+      for (int u = 0; u < nu; ++u) {
+        if (lane + 32 * u >= cnt) continue;
+        const Entry me = buf[lane + 32 * u];
+        int r = 0;
+        for (int j = 0; j < cnt; ++j) r += key_less(buf[j], me);
+        rank[u] = r;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u)
-      if (lane + 32 * u < cnt) out[rank[u]] = mine[u].member;
+      if (lane + 32 * u < cnt) out[rank[u]] = buf[lane + 32 * u].member;
+    if constexpr (ENV) env_rows(a, li, cnt, rank, buf);
   } else {
+    double sig = 0.0;
     for (int i = lane; i < cnt; i += 32) {
-      const NbrEntry me = buf[i];
+      const Entry me = buf[i];
       int rank = 0;
       for (int j = 0; j < cnt; ++j) rank += key_less(buf[j], me);
       out[rank] = me.member;
+      if constexpr (ENV) sig += env_row(a, li, rank, me);
+    }
+    if constexpr (ENV) {
+      sig = warp_sum(sig);
+      if (lane == 0) a.sig[li] = sig;
     }
   }
 }
@@ -396,9 +478,16 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
 void launch_neighbors(const NbrArgs& a, cudaStream_t st) {
   if (a.n_lists == 0) return;
   const int cap = ((a.n_max + 1 + 31) / 32) * 32;
-  const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry);
-  ensure_smem_attr(reinterpret_cast<const void*>(k_neighbors), smem);
-  k_neighbors<<<(a.n_lists + kNbrWarps - 1) / kNbrWarps, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
+  const int grid = (a.n_lists + kNbrWarps - 1) / kNbrWarps;
+  if (a.R) {
+    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntryEnv);
+    ensure_smem_attr(reinterpret_cast<const void*>(k_neighbors<true>), smem);
+    k_neighbors<true><<<grid, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
+  } else {
+    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry);
+    ensure_smem_attr(reinterpret_cast<const void*>(k_neighbors<false>), smem);
+    k_neighbors<false><<<grid, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
+  }
 }
 
 // ----------------------------------------------------------------------------------
@@ -469,51 +558,204 @@ void launch_force_gather(const ForceArgs& a, cudaStream_t st) {
   k_force_gather<<<static_cast<int>((threads + 127) / 128), 128, 0, st>>>(a); count_launch();
 }
 
-// Per-atom assembly: owner's zero-image partial first, then the ghost images of the atom
-// in shift order (the masked route, decomp.cpp:502-536); wide_halo keeps locals only.
-// Accumulates into the step output (virtual ranks run in ascending order).
-__global__ void k_assemble(AssembleArgs a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.n_atoms) return;
-  const int nloc = a.counts[0];
-  double f[3] = {0, 0, 0};
-  const bool mine = a.owner[i] == a.rank;
-  if (mine) {
-    const int m = a.loc_off[i];
-    for (int c = 0; c < 3; ++c) f[c] += a.fmem[3 * static_cast<size_t>(m) + c];
-    a.out[10 + 3 * static_cast<size_t>(a.n_atoms) + i] = a.e_centre[m];
+// ----------------------------------------------------------------------------------
+// Ghost-force route (masked_reduction, decomp.cpp:445-469, 502-536).
+// Pack, per DD rank: the owner's zero-image partial of each local goes to fown/eown
+// (global atom index; exactly one rank owns an atom), and every ghost image that received
+// partials becomes a RouteEntry for the atom's owner, grouped by destination rank.
+// ----------------------------------------------------------------------------------
+__global__ void k_route_count(RouteArgs a) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= a.nloc + a.ngh) return;
+  if (m < a.nloc) {
+    const int t = a.m_atom[m];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) a.fown[3 * static_cast<size_t>(t) + q] = a.fmem[3 * static_cast<size_t>(m) + q];
+    a.eown[t] = a.e_centre[m];
+  } else if (!a.wide && a.rn[m - a.nloc] > 0) {
+    atomicAdd(&a.cnt[a.rank * a.n_ranks + a.m_owner[m]], 1);
   }
-  if (!a.wide)
-    for (int m = nloc + a.gh_off[i]; m < nloc + a.gh_off[i + 1]; ++m)
-      for (int c = 0; c < 3; ++c) f[c] += a.fmem[3 * static_cast<size_t>(m) + c];
-  for (int c = 0; c < 3; ++c) a.out[10 + 3 * static_cast<size_t>(i) + c] += f[c];
 }
 
-void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
-  if (a.n_atoms == 0) return;
-  k_assemble<<<(a.n_atoms + 255) / 256, 256, 0, st>>>(a); count_launch();
+__global__ void k_route_fill(RouteArgs a) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= a.ngh || a.rn[g] == 0) return;
+  const int m = a.nloc + g;
+  const int o = a.m_owner[m];
+  const int* row = a.cnt + a.rank * a.n_ranks;
+  int off = 0;
+  for (int q = 0; q < o; ++q) off += row[q];
+  RouteEntry e;
+  e.atom = a.m_atom[m];
+  e.img = static_cast<short>(a.m_shift[m]);
+  e.src = static_cast<short>(a.rank);
+#pragma unroll
+  for (int q = 0; q < 3; ++q) e.f[q] = a.fmem[3 * static_cast<size_t>(m) + q];
+  a.buf[off + atomicAdd(&a.cur[o], 1)] = e;
 }
+
+void launch_route_pack(const RouteArgs& a, cudaStream_t st) {
+  const int nm = a.nloc + a.ngh;
+  if (nm > 0) {
+    k_route_count<<<(nm + 255) / 256, 256, 0, st>>>(a); count_launch();
+  }
+  if (!a.wide && a.ngh > 0) {
+    k_route_fill<<<(a.ngh + 255) / 256, 256, 0, st>>>(a); count_launch();
+  }
+}
+
+// Merge.  Segment (s, o) = entries from source rank s for a destination o owned by this
+// process; s's entries sit in its send buffer (s local: every destination, grouped) or in
+// its receive buffer (s remote: this process's destinations only, grouped).
+__device__ __forceinline__ bool rank_is_local(const MergeArgs& a, int r) {
+  return r % a.world_size == a.world_rank;
+}
+
+__global__ void k_merge_plan(MergeArgs a) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int R = a.n_ranks;
+  int* prefix = a.seg;            // [R*R + 1]
+  int* offset = a.seg + R * R + 1;  // [R*R]
+  int tot = 0;
+  for (int s = 0; s < R; ++s) {
+    const bool sl = rank_is_local(a, s);
+    int off = 0;
+    for (int o = 0; o < R; ++o) {
+      const int c = a.cnt[s * R + o];
+      const bool ol = rank_is_local(a, o);
+      prefix[s * R + o] = tot;
+      offset[s * R + o] = off;
+      if (ol) tot += c;
+      if (sl || ol) off += c;
+    }
+  }
+  prefix[R * R] = tot;
+}
+
+// entry i of the incoming stream (segments in (s, o) order), nullptr past the end
+__device__ __forceinline__ const RouteEntry* merge_entry(const MergeArgs& a, int i) {
+  const int R = a.n_ranks;
+  const int* prefix = a.seg;
+  if (i >= prefix[R * R]) return nullptr;
+  int lo = 0, hi = R * R;  // largest q with prefix[q] <= i and a non-empty segment
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (prefix[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  const int s = lo / R;
+  return a.src_base[s] + a.seg[R * R + 1 + lo] + (i - prefix[lo]);
+}
+
+__global__ void k_merge_count(MergeArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.capacity) return;
+  const RouteEntry* e = merge_entry(a, i);
+  if (e) atomicAdd(&a.inc_cnt[e->atom], 1);
+}
+
+__global__ void k_merge_fill(MergeArgs a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.capacity) return;
+  const RouteEntry* e = merge_entry(a, i);
+  if (e) a.inc[a.inc_off[e->atom] + atomicSub(&a.inc_cnt[e->atom], 1) - 1] = e;
+}
+
+// Thread per atom owned by this process: own zero-image partial, then the routed partials
+// in (zero image first, image, rank) order -- a unique key per entry, so the sum does not
+// depend on the arrival order.
+__global__ void k_merge_sum(MergeArgs a) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.n_atoms || !rank_is_local(a, a.owner[t])) return;
+  double f[3] = {a.fown[3 * static_cast<size_t>(t)], a.fown[3 * static_cast<size_t>(t) + 1],
+                 a.fown[3 * static_cast<size_t>(t) + 2]};
+  const int b = a.inc_off[t], e = a.inc_off[t + 1];
+  auto key = [](const RouteEntry* r) {
+    return ((r->img == kZeroShift ? 0 : 1) << 24) | (static_cast<int>(r->img) << 16) | static_cast<int>(r->src);
+  };
+  int prev = -1;
+  for (int done = b; done < e; ++done) {
+    const RouteEntry* best = nullptr;
+    int bk = 0x7fffffff;
+    for (int j = b; j < e; ++j) {
+      const int k = key(a.inc[j]);
+      if (k > prev && k < bk) {
+        bk = k;
+        best = a.inc[j];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) f[q] += best->f[q];
+    prev = bk;
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) a.f_out[3 * static_cast<size_t>(t) + q] = f[q];
+}
+
+void launch_route_merge(const MergeArgs& a, cudaStream_t st) {
+  k_merge_plan<<<1, 32, 0, st>>>(a); count_launch();
+  if (a.capacity > 0) {
+    k_merge_count<<<(a.capacity + 255) / 256, 256, 0, st>>>(a); count_launch();
+    launch_scan(a.inc_cnt, a.inc_off, a.n_atoms, st);
+    k_merge_fill<<<(a.capacity + 255) / 256, 256, 0, st>>>(a); count_launch();
+  } else {
+    cudaMemsetAsync(a.inc_off, 0, (a.n_atoms + 1) * sizeof(int), st);
+  }
+  if (a.n_atoms > 0) {
+    k_merge_sum<<<(a.n_atoms + 255) / 256, 256, 0, st>>>(a); count_launch();
+  }
+}
+
+__global__ void k_finalize(const double* __restrict__ red, int R, long n, double* __restrict__ out) {
+  const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (i < 10) {
+    double v = 0.0;
+    for (int r = 0; r < R; ++r) v += red[10 * r + i];
+    out[i] = v;
+  }
+  if (i < 4 * n) out[10 + i] = red[10 * static_cast<long>(R) + i];
+}
+
+void launch_finalize(const double* red, int n_ranks, long n_atoms, double* out, cudaStream_t st) {
+  const long tot = std::max(10L, 4 * n_atoms);
+  k_finalize<<<static_cast<int>((tot + 255) / 256), 256, 0, st>>>(red, n_ranks, n_atoms, out); count_launch();
+}
+
+// Two-stage deterministic reduction: block b sums the centres of its contiguous chunk
+// (fixed thread order + block_sum tree), then one block adds the block partials in order.
+constexpr int kEvBlocks = 148;
 
 __global__ void __launch_bounds__(256) k_energy_virial(const double* __restrict__ e,
                                                        const double* __restrict__ vir,
                                                        const int* __restrict__ counts,
-                                                       double* __restrict__ out) {
+                                                       double* __restrict__ part) {
   __shared__ double red[8];
   const int nloc = counts[0];
+  const int chunk = (nloc + gridDim.x - 1) / gridDim.x;
+  const int c0 = blockIdx.x * chunk, c1 = min(nloc, c0 + chunk);
   double acc[10] = {0};
-  for (int c = threadIdx.x; c < nloc; c += blockDim.x) {
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
     acc[0] += e[c];
     for (int q = 0; q < 9; ++q) acc[1 + q] += vir[9 * static_cast<size_t>(c) + q];
   }
   for (int q = 0; q < 10; ++q) {
     const double t = block_sum(acc[q], red);
-    if (threadIdx.x == 0) out[q] += t;
+    if (threadIdx.x == 0) part[10 * blockIdx.x + q] = t;
   }
 }
 
-void launch_energy_virial(const double* e, const double* vir, const int* counts, double* out,
+__global__ void k_energy_virial_final(const double* __restrict__ part, int nb, double* __restrict__ row) {
+  const int q = threadIdx.x;
+  if (q >= 10) return;
+  double t = 0.0;
+  for (int b = 0; b < nb; ++b) t += part[10 * b + q];
+  row[q] = t;
+}
+
+void launch_energy_virial(const double* e, const double* vir, const int* counts, double* part, double* row,
                           cudaStream_t st) {
-  k_energy_virial<<<1, 256, 0, st>>>(e, vir, counts, out); count_launch();
+  k_energy_virial<<<kEvBlocks, 256, 0, st>>>(e, vir, counts, part); count_launch();
+  k_energy_virial_final<<<1, 32, 0, st>>>(part, kEvBlocks, row); count_launch();
 }
 
 }  // namespace nb

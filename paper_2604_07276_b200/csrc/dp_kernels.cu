@@ -236,7 +236,8 @@ struct CentreQueue {
   }
 };
 
-// Stage centre c's env rows (written by k_env) into shared memory; returns sigma.
+// Stage centre c's env rows (written by the centre-list build, k_neighbors) into shared
+// memory; returns sigma.
 __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int& zi) {
   zi = a.species[a.m_atom[a.cen_member[c]]];
   const float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
@@ -1043,46 +1044,6 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   mm.finish();
 }
 
-// ------------------------------------------------------------------------------------
-// Environment matrix (prepare_rows + switch_eval, dp_core.hpp:116-137, 200-223): warp
-// per centre, lanes over its rows.  d = image_delta(...) and r, s, ds/dr in exact FP64,
-// env row R = (s, s/r d) stored as float4 (coalesced 16-byte stores), neighbour species,
-// and sigma = sum_k s_k^2 (FP64, fixed-order warp reduction).
-// ------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_env(const __grid_constant__ DpArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= a.n_centres) return;
-  const int n = a.nn[c];
-  const int cm = a.cen_member[c];
-  const int ca = a.m_atom[cm];
-  const int cs = a.m_shift[cm];
-  const double pc[3] = {a.pos[3 * ca], a.pos[3 * ca + 1], a.pos[3 * ca + 2]};
-  const int* list = a.nlist + static_cast<size_t>(c) * a.n_max;
-  float4* R = a.R + static_cast<size_t>(c) * a.n_max;
-  int* Z = a.Z + static_cast<size_t>(c) * a.n_max;
-  double sig = 0.0;
-  for (int k = lane; k < n; k += 32) {
-    const int mj = list[k];
-    const int aj = a.m_atom[mj];
-    const int sj = a.m_shift[mj];
-    const int rel[3] = {shift_x(sj) - shift_x(cs), shift_y(sj) - shift_y(cs), shift_z(sj) - shift_z(cs)};
-    double d[3];
-#pragma unroll
-    for (int q = 0; q < 3; ++q) d[q] = image_delta(a.pos[3 * aj + q], pc[q], rel[q], a.L[q]);
-    const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
-    double sw, ds;
-    switch_fn(r, a.rcs, a.rc, sw, ds);
-    const double sr = sw / r;
-    R[k] = make_float4(static_cast<float>(sw), static_cast<float>(sr * d[0]), static_cast<float>(sr * d[1]),
-                       static_cast<float>(sr * d[2]));
-    Z[k] = a.species[aj];
-    sig += sw * sw;
-  }
-  sig = warp_sum(sig);
-  if (lane == 0) a.sig[c] = sig;
-}
-
 // Pre-split weight image of a GEMM's B operand (tc::bulk_g2s): B(k, n) = TB ? W[n*ldb + k]
 // : W[k*ldb + n], K x N, per 32-wide K chunk [hi | lo] of NT rows x 128 bytes, K-major
 // SW128.  Built once per context; the per-centre GEMMs then stage it with two bulk copies.
@@ -1118,12 +1079,6 @@ void launch_weight_image(const float* W, int TB, int ldb, int K, int N, uint8_t*
   count_launch();
 }
 
-void launch_env(const DpArgs& a, cudaStream_t st) {
-  if (a.n_centres == 0) return;
-  const long threads = static_cast<long>(a.n_centres) * 32;
-  k_env<<<static_cast<int>((threads + 255) / 256), 256, 0, st>>>(a);
-  count_launch();
-}
 
 template <int MODE, bool WIMG>
 static void set_smem(size_t smem) {

@@ -93,6 +93,12 @@ struct NbrArgs {
   int* err;                  // &err[slot]: atomicMin of the owner atom of an overflowing list
   int* nonempty;             // optional: count of lists with >= 1 row (route entries)
   int* maxn;                 // optional: atomicMax of the row counts
+  uint64_t kbase;            // sort-key packing: bits(r2) - kbase < 2^58 for r2 < rc2
+  // fused environment matrix (centre lists only; NULL R: rows only)
+  float4* R;                 // [n_lists][n_max] (s, s/r d)
+  int* Z;                    // [n_lists][n_max] neighbour species
+  double* sig;               // [n_lists] sum_k s_k^2
+  double rc, rcs;
 };
 void launch_neighbors(const NbrArgs& a, cudaStream_t st);
 
@@ -111,22 +117,66 @@ struct ForceArgs {
 };
 void launch_force_gather(const ForceArgs& a, cudaStream_t st);
 
-struct AssembleArgs {
-  int n_atoms;
-  int rank;
-  int wide;
-  const int* owner;
-  const int* loc_off;    // exclusive prefix of locals per atom
-  const int* gh_off;     // exclusive prefix of ghosts per atom (n+1 entries)
-  const int* counts;     // [nloc, ngh]
-  const double* fmem;
-  const double* e_centre;  // centre energies
-  double* out;           // [E, W9, F(3n), ae(n)]
+// row[0..9] = [sum_{c < nloc} e[c], sum vir[c]] of one DD rank (deterministic single-block
+// reduction in two stages); the ranks' rows are summed in rank order by launch_finalize
+// part: scratch of kEnergyVirialPartials doubles
+constexpr int kEnergyVirialPartials = 148 * 10;
+void launch_energy_virial(const double* e_centre, const double* vir, const int* counts, double* part,
+                          double* row, cudaStream_t st);
+
+// ---------------------------------------------------------------- ghost-force route -----
+// One routed partial (decomp.cpp:445-455): a ghost image's force partial travelling from
+// the rank that evaluated it (src) to the atom's owner.  f is the force contribution
+// (the negated row-gradient partial), so the owner's merge is a plain sum.
+struct RouteEntry {
+  int atom;
+  short img;   // packed shift 0..26 (kZeroShift = 13)
+  short src;   // DD rank that evaluated the image
+  double f[3];
 };
-void launch_assemble(const AssembleArgs& a, cudaStream_t st);
-// E += sum_{c < nloc} e[c]; W += sum vir[c]  (deterministic single-block reduction)
-void launch_energy_virial(const double* e_centre, const double* vir, const int* counts,
-                          double* out, cudaStream_t st);
+static_assert(sizeof(RouteEntry) == 32, "RouteEntry is 32 bytes");
+
+struct RouteArgs {
+  int rank, n_ranks, wide;
+  int nloc, ngh;
+  const int* m_atom;
+  const int* m_shift;
+  const int* m_owner;
+  const int* rn;            // reverse-list row counts of the ghosts (0: no partials)
+  const double* fmem;       // [member][3] force partials of this rank
+  const double* e_centre;   // energies of the rank's centres (locals first)
+  double* fown;             // [n][3] owner's zero-image partial (global atom index)
+  double* eown;             // [n] atom energies (owner)
+  int* cnt;                 // [R][R] routed entries src -> dst (row = this rank)
+  int* cur;                 // [R] fill cursors of this rank (zeroed by count)
+  RouteEntry* buf;          // this rank's entries, grouped by destination (capacity ngh)
+};
+// base partials + per-destination counts, then the grouped fill (order inside a group is
+// not deterministic; the owner's merge orders entries by (zero image first, image, rank))
+void launch_route_pack(const RouteArgs& a, cudaStream_t st);
+
+constexpr int kMaxRanks = 64;
+struct MergeArgs {
+  int n_ranks, world_size, world_rank, n_atoms;
+  const int* cnt;                 // [R][R]
+  const RouteEntry* src_base[kMaxRanks];  // entries of source s: its send buffer (local s,
+                                          // grouped by every destination) or its receive
+                                          // buffer (remote s, this process's destinations)
+  int* seg;                       // scratch: [R*R + 1] segment prefix, [R*R] offsets
+  int* inc_cnt;                   // [n + 1] incoming entries per atom (zeroed by plan)
+  int* inc_off;                   // [n + 1] exclusive prefix
+  const RouteEntry** inc;         // [capacity] entries sorted by atom
+  int capacity;                   // >= total incoming entries
+  const int* owner;               // [n] owner rank of each atom
+  const double* fown;             // [n][3]
+  double* f_out;                  // [n][3] merged force of the locally owned atoms
+};
+// owner merge (decomp.cpp:502-536): own zero-image partial first, then the routed partials
+// in (zero image first, image, rank) order
+void launch_route_merge(const MergeArgs& a, cudaStream_t st);
+
+// out[0..9] = sum over ranks of row[r][0..9] in rank order; out[10..] = red[10R..] (F, e_i)
+void launch_finalize(const double* red, int n_ranks, long n_atoms, double* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- network -------------
 constexpr int kMaxLayers = 8;
@@ -166,9 +216,9 @@ struct DpArgs {
   float* PTst;
   float* EMBst;
   size_t u_layer_stride, p_layer_stride, emb_centre_stride;
-  float4* R;            // [n_centres][n_max] env rows (s, s dx/r, s dy/r, s dz/r), k_env
-  int* Z;               // [n_centres][n_max] neighbour species, k_env
-  double* sig;          // [n_centres] sum_k s_k^2 (FP64), k_env
+  float4* R;            // [n_centres][n_max] env rows (s, s dx/r, s dy/r, s dz/r), k_neighbors
+  int* Z;               // [n_centres][n_max] neighbour species, k_neighbors
+  double* sig;          // [n_centres] sum_k s_k^2 (FP64), k_neighbors
   float* Ad;            // [n_centres][M*4]
   float* Bd;            // [n_centres][4*mr]
   float* D;             // [n_centres][M*mr]
@@ -198,7 +248,6 @@ size_t dp_scratch_floats(const DpArgs& a);
 size_t dp_smem_bytes(const DpArgs& a, int mode);
 // Environment matrix: FP64 geometry (image_delta, r, switch) -> float4 env rows, species,
 // and sigma = sum s^2 per centre; warp per centre, coalesced row stores.
-void launch_env(const DpArgs& a, cudaStream_t st);
 void launch_centre_forward(const DpArgs& a, int grid, cudaStream_t st);
 void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st);
 
