@@ -608,8 +608,6 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.n_centres = ncen;
   dp.nlist = nlist_.p;
   dp.nn = nn_.p;
-  dp.x_layer_stride = static_cast<size_t>(ncen) * nmax * M;
-  X_.ensure(dp.x_layer_stride * (m.na + 1) + 4);
   Ad_.ensure(static_cast<size_t>(ncen) * M * 4 + 4);
   Bd_.ensure(static_cast<size_t>(ncen) * 4 * mr + 4);
   D_.ensure(static_cast<size_t>(ncen) * M * mr + 4);
@@ -617,25 +615,8 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   g_.ensure(static_cast<size_t>(ncen) * nmax * 3 + 3);
   vir_.ensure(static_cast<size_t>(ncen) * 9 + 9);
   e_.ensure(ncen + 1);
-  {
-    const size_t nm4 = (static_cast<size_t>(nmax) + 3) & ~size_t(3);
-    dp.u_layer_stride = static_cast<size_t>(ncen) * nmax * 2 * M;
-    dp.p_layer_stride = static_cast<size_t>(ncen) * nmax * nm4;
-    size_t ew = 0;
-    for (int e = 0; e + 1 < dp.n_embed; ++e) ew += static_cast<size_t>(dp.edims[e]);
-    dp.emb_centre_stride = static_cast<size_t>(nmax) * ew;
-    Ust_.ensure(dp.u_layer_stride * std::max(1, m.na) + 4);
-    PUst_.ensure(dp.p_layer_stride * std::max(1, m.na) + 4);
-    PTst_.ensure(dp.p_layer_stride * std::max(1, m.na) + 4);
-    EMBst_.ensure(dp.emb_centre_stride * ncen + 4);
-    dp.Ust = Ust_.p;
-    dp.PUst = PUst_.p;
-    dp.PTst = PTst_.p;
-    dp.EMBst = EMBst_.p;
-  }
   dp.Z = Z_.p;
   dp.sig = sig_.p;
-  dp.X = X_.p;
   dp.R = R_.p;
   dp.Ad = Ad_.p;
   dp.Bd = Bd_.p;
@@ -643,7 +624,8 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.dD = dD_.p;
   dp.g = g_.p;
   dp.vir = vir_.p;
-  static const int flags = getenv("NNMD_FLAGS") ? atoi(getenv("NNMD_FLAGS")) : 0;
+  // diagnostic switches, read per call (tests toggle bit 3, multi-centre units)
+  const int flags = getenv("NNMD_FLAGS") ? atoi(getenv("NNMD_FLAGS")) : 0;
   dp.flags = flags;
   if (!(flags & 4) && wimg_.p) {  // bit 2: stage weights through registers instead
     auto img = [&](long off) -> const uint8_t* { return off >= 0 ? wimg_.p + off : nullptr; };
@@ -663,7 +645,44 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.mode = opts_.precision == NNMD_PREC_FP32 ? 1 : opts_.precision == NNMD_PREC_TF32 ? 2 : 0;
   work_.ensure(1);
   dp.work = work_.p;
-  const int grid = std::max(1, std::min(ncen, 2 * n_sm_));  // two CTAs per SM (SIMT and tcgen05)
+  // work units: one centre each, or (n_max <= 64, tcgen05 + weight images) packs of up to
+  // four consecutive centres in one 128-row tile (NNMD_FLAGS bit 3 disables packing)
+  const bool pack = dp.mode != 0 && dp.wimg && nmax <= 64 && !(flags & 8);
+  int units = ncen;
+  dp.unit_rows = nmax;
+  if (pack && ncen > 0) {
+    units = pack_capacity(ncen);
+    const int ng = (ncen + 3) / 4;
+    pack_cnt_.ensure(2 * static_cast<size_t>(ng) + 2);
+    packs_.ensure(static_cast<size_t>(units) + 1);
+    tic("pack_plan");
+    launch_pack_plan(nn_.p, ncen, pack_cnt_.p, pack_cnt_.p + ng + 1, packs_.p, st_);
+    toc();
+    dp.packs = packs_.p;
+    dp.n_units_dev = pack_cnt_.p + ng + 1 + ng;
+    dp.unit_rows = 128;
+  }
+  {
+    const size_t ur = static_cast<size_t>(dp.unit_rows);
+    const size_t ur4 = (ur + 3) & ~size_t(3);
+    dp.x_layer_stride = static_cast<size_t>(units) * ur * M;
+    X_.ensure(dp.x_layer_stride * (m.na + 1) + 4);
+    dp.u_layer_stride = static_cast<size_t>(units) * ur * 2 * M;
+    dp.p_layer_stride = static_cast<size_t>(units) * ur * ur4;
+    size_t ew = 0;
+    for (int e = 0; e + 1 < dp.n_embed; ++e) ew += static_cast<size_t>(dp.edims[e]);
+    dp.emb_centre_stride = ur * ew;
+    Ust_.ensure(dp.u_layer_stride * std::max(1, m.na) + 4);
+    PUst_.ensure(dp.p_layer_stride * std::max(1, m.na) + 4);
+    PTst_.ensure(dp.p_layer_stride * std::max(1, m.na) + 4);
+    EMBst_.ensure(dp.emb_centre_stride * units + 4);
+    dp.X = X_.p;
+    dp.Ust = Ust_.p;
+    dp.PUst = PUst_.p;
+    dp.PTst = PTst_.p;
+    dp.EMBst = EMBst_.p;
+  }
+  const int grid = std::max(1, std::min(units, 2 * n_sm_));  // two CTAs per SM (SIMT and tcgen05)
   dp.scratch_slot = (dp_scratch_floats(dp) + 31) & ~size_t(31);
   scratch_.ensure(dp.scratch_slot * grid);
   dp.scratch = scratch_.p;

@@ -153,6 +153,8 @@ class Context {
   DevBuf<float4> R_;
   DevBuf<double> g_, vir_, e_, fmem_, sig_;
   DevBuf<int> Z_;
+  DevBuf<int> pack_cnt_;   // pack plan: per-group unit counts | their exclusive scan (+ total)
+  DevBuf<int2> packs_;     // (first centre, centre count) per unit
   // ghost-force route and the step result (decomp.cpp:445-538)
   DevBuf<double> red_;    // [R][10] per-rank [E, W9] rows | F [n][3] | e_i [n]  (reduced)
   DevBuf<double> fown_;   // [n][3] owner's zero-image partial

@@ -721,6 +721,46 @@ void launch_finalize(const double* red, int n_ranks, long n_atoms, double* out, 
   k_finalize<<<static_cast<int>((tot + 255) / 256), 256, 0, st>>>(red, n_ranks, n_atoms, out); count_launch();
 }
 
+// ----------------------------------------------------------------------------------
+// Multi-centre tiles (rc = 4: n <= 64, ~27 rows per centre): groups of four consecutive
+// centres become one 128-row unit when their rows fit, else two pairs (always fit).
+// ----------------------------------------------------------------------------------
+__device__ __forceinline__ int pack_group_units(const int* nn, int n_centres, int g) {
+  const int c0 = 4 * g, c1 = min(n_centres, c0 + 4);
+  int rows = 0;
+  for (int c = c0; c < c1; ++c) rows += nn[c];
+  return (rows <= 128 || c1 - c0 <= 2) ? 1 : 2;
+}
+
+__global__ void k_pack_count(const int* __restrict__ nn, int n_centres, int* __restrict__ cnt) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < (n_centres + 3) / 4) cnt[g] = pack_group_units(nn, n_centres, g);
+}
+
+__global__ void k_pack_fill(const int* __restrict__ nn, int n_centres, const int* __restrict__ off,
+                            int2* __restrict__ packs) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (n_centres + 3) / 4) return;
+  const int c0 = 4 * g, m = min(4, n_centres - c0);
+  if (pack_group_units(nn, n_centres, g) == 1) {
+    packs[off[g]] = make_int2(c0, m);
+  } else {
+    packs[off[g]] = make_int2(c0, 2);
+    packs[off[g] + 1] = make_int2(c0 + 2, m - 2);
+  }
+}
+
+void launch_pack_plan(const int* nn, int n_centres, int* cnt, int* off, int2* packs, cudaStream_t st) {
+  const int ng = (n_centres + 3) / 4;
+  if (ng == 0) {
+    cudaMemsetAsync(off, 0, sizeof(int), st);
+    return;
+  }
+  k_pack_count<<<(ng + 255) / 256, 256, 0, st>>>(nn, n_centres, cnt); count_launch();
+  launch_scan(cnt, off, ng, st);  // off[ng] = unit count
+  k_pack_fill<<<(ng + 255) / 256, 256, 0, st>>>(nn, n_centres, off, packs); count_launch();
+}
+
 // Two-stage deterministic reduction: block b sums the centres of its contiguous chunk
 // (fixed thread order + block_sum tree), then one block adds the block partials in order.
 constexpr int kEvBlocks = 148;

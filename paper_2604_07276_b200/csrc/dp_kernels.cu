@@ -40,7 +40,7 @@ __host__ __device__ inline int max_width(const DpArgs& a) {
 
 __host__ __device__ inline size_t emb_floats(const DpArgs& a) {
   size_t t = 0;
-  for (int e = 0; e + 1 < a.n_embed; ++e) t += static_cast<size_t>(a.n_max) * a.edims[e];
+  for (int e = 0; e + 1 < a.n_embed; ++e) t += static_cast<size_t>(a.unit_rows) * a.edims[e];
   return t;
 }
 
@@ -144,6 +144,13 @@ struct Smem {
   int* z;
   double* red;
   unsigned char* part;  // column-pass partials: [2][n_max] float4 + [2][n_max] float
+  // multi-centre units (DpArgs::packs): the unit's centres and, per row, its centre
+  int* pk_cen;          // [4] centre index
+  int* pk_off;          // [5] row offsets
+  float* pk_isig;       // [4] 1 / sigma
+  int* pk_zi;           // [4] centre species
+  float* pk_dsig;       // [4] dsigma (backward)
+  int* rcen;            // [unit_rows] local centre of each row
 };
 
 __host__ __device__ inline size_t smem_layout(const DpArgs& a, int mode, unsigned char* base, Smem* out) {
@@ -155,22 +162,36 @@ __host__ __device__ inline size_t smem_layout(const DpArgs& a, int mode, unsigne
     return p;
   };
   Smem s;
+  const int ur = a.unit_rows;
   s.head = take(head_bytes(mode));
-  s.R = reinterpret_cast<float4*>(take(sizeof(float4) * a.n_max));
-  s.dR = reinterpret_cast<float4*>(take(sizeof(float4) * a.n_max));
-  s.s = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
-  s.dsx = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
-  s.t = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
-  s.rowpart = reinterpret_cast<float*>(take(sizeof(float) * a.n_max));
+  s.R = reinterpret_cast<float4*>(take(sizeof(float4) * ur));
+  s.dR = reinterpret_cast<float4*>(take(sizeof(float4) * ur));
+  s.s = reinterpret_cast<float*>(take(sizeof(float) * ur));
+  s.dsx = reinterpret_cast<float*>(take(sizeof(float) * ur));
+  s.t = reinterpret_cast<float*>(take(sizeof(float) * ur));
+  s.rowpart = reinterpret_cast<float*>(take(sizeof(float) * ur));
   s.Ad = reinterpret_cast<float*>(take(sizeof(float) * a.M * 4));
   s.Bd = reinterpret_cast<float*>(take(sizeof(float) * 4 * a.mr));
   s.dAd = reinterpret_cast<float*>(take(sizeof(float) * a.M * 4));
   s.dBd = reinterpret_cast<float*>(take(sizeof(float) * 4 * a.mr));
-  s.z = reinterpret_cast<int*>(take(sizeof(int) * a.n_max));
+  s.z = reinterpret_cast<int*>(take(sizeof(int) * ur));
   s.red = reinterpret_cast<double*>(take(sizeof(double) * 32));
+  // multi-centre units only (the single-centre kernels sit at the two-CTAs-per-SM shared
+  // memory limit at n_max = 160: no bytes to spare there)
+  if (a.packs) {
+    s.pk_cen = reinterpret_cast<int*>(take(sizeof(int) * 4));
+    s.pk_off = reinterpret_cast<int*>(take(sizeof(int) * 5));
+    s.pk_isig = reinterpret_cast<float*>(take(sizeof(float) * 4));
+    s.pk_zi = reinterpret_cast<int*>(take(sizeof(int) * 4));
+    s.pk_dsig = reinterpret_cast<float*>(take(sizeof(float) * 4));
+    s.rcen = reinterpret_cast<int*>(take(sizeof(int) * ur));
+  } else {
+    s.pk_cen = s.pk_off = s.pk_zi = s.rcen = nullptr;
+    s.pk_isig = s.pk_dsig = nullptr;
+  }
   // tcgen05 modes park the column-pass partials in the (idle) 96 KB operand stage; the
   // SIMT head (one 64x64 tile) is too small, so it gets its own region
-  s.part = mode == 0 ? take(static_cast<size_t>(a.n_max) * 2 * (sizeof(float4) + sizeof(float))) : s.head;
+  s.part = mode == 0 ? take(static_cast<size_t>(ur) * 2 * (sizeof(float4) + sizeof(float))) : s.head;
   if (out) *out = s;
   return o;
 }
@@ -252,20 +273,57 @@ __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int
   return a.sig[c];
 }
 
+// Stage multi-centre unit u (DpArgs::packs): its centres, their row offsets, 1/sigma, the
+// centre species and, for every row, its env row, neighbour species and local centre.
+// Returns the unit's row count (<= 128).
+__device__ int unit_rows_pack(const DpArgs& a, int u, const Smem& sm) {
+  if (threadIdx.x == 0) {
+    const int2 pk = a.packs[u];
+    int off = 0;
+    for (int i = 0; i < 4; ++i) {
+      const bool v = i < pk.y;
+      const int c = pk.x + i;
+      sm.pk_cen[i] = v ? c : -1;
+      sm.pk_off[i] = off;
+      const double sg = v ? a.sig[c] : 0.0;
+      sm.pk_isig[i] = sg > 0.0 ? static_cast<float>(1.0 / sg) : 0.f;
+      sm.pk_zi[i] = v ? a.species[a.m_atom[a.cen_member[c]]] : 0;
+      off += v ? a.nn[c] : 0;
+    }
+    sm.pk_off[4] = off;
+  }
+  __syncthreads();
+  for (int i = 0; i < 4 && sm.pk_cen[i] >= 0; ++i) {
+    const int c = sm.pk_cen[i], o = sm.pk_off[i], n = sm.pk_off[i + 1] - o;
+    const float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
+    const int* Zg = a.Z + static_cast<size_t>(c) * a.n_max;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const float4 R = Rg[k];
+      sm.R[o + k] = R;
+      sm.s[o + k] = R.x;
+      sm.z[o + k] = Zg[k];
+      sm.rcen[o + k] = i;
+    }
+  }
+  __syncthreads();
+  return sm.pk_off[4];
+}
+
 // Embedding net over the n rows: layer 0 folded (s*w0 + ctab[zj][zi]), then tanh layers.
 // Writes intermediate activations to EMB and the last to `out` (n x M).
-template <int MODE, bool WIMG, class MmT>
+template <int MODE, bool WIMG, bool PACK = false, class MmT>
 __device__ void embed_forward(MmT& mm, const DpArgs& a, int n, int zi, const Smem& sm, float* emb,
                               float* out) {
   const int E0 = a.edims[0];
   float* cur = (a.n_embed == 1) ? out : emb;
   for (int idx = threadIdx.x; idx < n * E0; idx += blockDim.x) {
     const int k = idx / E0, o = idx - k * E0;
-    const float v = fmaf(sm.s[k], a.w0[o], a.ctab[(static_cast<size_t>(sm.z[k]) * a.ns + zi) * E0 + o]);
+    const int zc = PACK ? sm.pk_zi[sm.rcen[k]] : zi;  // the row's centre species
+    const float v = fmaf(sm.s[k], a.w0[o], a.ctab[(static_cast<size_t>(sm.z[k]) * a.ns + zc) * E0 + o]);
     cur[idx] = tanhf(v);
   }
   __syncthreads();
-  size_t off = static_cast<size_t>(a.n_max) * E0;
+  size_t off = static_cast<size_t>(a.unit_rows) * E0;
   for (int e = 1; e < a.n_embed; ++e) {
     const int Ein = a.edims[e - 1], Eout = a.edims[e];
     float* nxt = (e + 1 == a.n_embed) ? out : emb + off;
@@ -275,13 +333,15 @@ __device__ void embed_forward(MmT& mm, const DpArgs& a, int n, int zi, const Sme
                                              a.img_ew[e]);
     __syncthreads();
     cur = nxt;
-    off += static_cast<size_t>(a.n_max) * Eout;
+    off += static_cast<size_t>(a.unit_rows) * Eout;
   }
 }
 
 // Register-cached rows (n <= 32 C): each lane keeps its C key columns' s_j^2 and R_j for
 // all of its warp's rows.
-template <int C>
+// PACK: rows of a multi-centre unit only see their own centre's columns (block-diagonal
+// S); pu and P~ are written as zero outside the block so the PV product stays exact.
+template <int C, bool PACK = false>
 __device__ void softmax_gate_rc(int n, int ln, const float* S, int lds, float* PU, float* PT, float inv_sig,
                                 const Smem& sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -295,12 +355,19 @@ __device__ void softmax_gate_rc(int n, int ln, const float* S, int lds, float* P
   }
   for (int k = wid; k < n; k += nw) {
     const float* row = S + static_cast<size_t>(k) * lds;
+    int jb = 0, je = n;
+    if constexpr (PACK) {
+      const int i = sm.rcen[k];
+      jb = sm.pk_off[i];
+      je = sm.pk_off[i + 1];
+      inv_sig = sm.pk_isig[i];
+    }
     float e[C];
     float mx = -FLT_MAX;
 #pragma unroll
     for (int t = 0; t < C; ++t) {
       const int j = lane + 32 * t;
-      e[t] = j < n ? row[j] : -FLT_MAX;
+      e[t] = (j >= jb && j < je) ? row[j] : -FLT_MAX;
       mx = fmaxf(mx, e[t]);
     }
     mx = warp_max(mx);
@@ -308,7 +375,7 @@ __device__ void softmax_gate_rc(int n, int ln, const float* S, int lds, float* P
 #pragma unroll
     for (int t = 0; t < C; ++t) {
       const int j = lane + 32 * t;
-      e[t] = j < n ? __expf(e[t] - mx) : 0.f;
+      e[t] = (j >= jb && j < je) ? __expf(e[t] - mx) : 0.f;
       den += s2[t] * e[t];
     }
     den = warp_sum(den);
@@ -481,6 +548,10 @@ __device__ void bwd_col_pass(int n, int ln, int stride, const float* TS, int ldt
 // reduced once.  After t_k is reduced the row's dS is written from the same registers, so
 // dP~ and pu are read once.  Same results as bwd_row_pass + bwd_col_pass up to summation
 // order.
+// PACK: multi-centre unit -- each row only pairs with its own centre's columns (the
+// tile and the stash hold other centres' junk off the diagonal blocks, masked here, so dS
+// is zero there), 1/sigma per centre, and dsigma summed per centre.
+template <bool PACK = false>
 __device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float* __restrict__ PU, float* DS,
                             float inv_sig, const Smem& sm, unsigned char* part_raw) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -504,6 +575,14 @@ __device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float
   float dsg = 0.f;
   for (int k = wid; k < n; k += nw) {
     const float4 Rk = sm.R[k];
+    int jb = 0, je = n;
+    if constexpr (PACK) {
+      const int i = sm.rcen[k];
+      jb = sm.pk_off[i];
+      je = sm.pk_off[i + 1];
+      inv_sig = sm.pk_isig[i];
+      dsg = 0.f;
+    }
     float4 tv = make_float4(0.f, 0.f, 0.f, 0.f), pu = tv;
     if (act) {
       tv = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(k) * ldt + j4);
@@ -515,7 +594,7 @@ __device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float
     float t = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const bool v = j4 + q < n;
+      const bool v = j4 + q >= jb && j4 + q < je;
       const float tt = v ? tq[q] : 0.f;  // the tile and stash hold junk past column n
       pq[q] = v ? pq[q] : 0.f;
       const float C = dot4(Rk, Rj[q]);
@@ -557,9 +636,15 @@ __device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float
       ds[q] = sj2[q] * pq[q] * dpt;
     }
     if (act) *reinterpret_cast<float4*>(DS + static_cast<size_t>(k) * ln + j4) = make_float4(ds[0], ds[1], ds[2], ds[3]);
+    if constexpr (PACK) {
+      dsg = warp_sum(dsg);
+      if (lane == 0) sm.rowpart[k] = dsg;
+    }
   }
-  dsg = warp_sum(dsg);
-  if (lane == 0) sm.red[8 + wid] = dsg;
+  if constexpr (!PACK) {
+    dsg = warp_sum(dsg);
+    if (lane == 0) sm.red[8 + wid] = dsg;
+  }
   if (act) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -569,8 +654,19 @@ __device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float
   }
   __syncthreads();
   float dsig = 0.f;
-  for (int w = 0; w < nw; ++w) dsig += static_cast<float>(sm.red[8 + w]);
+  if constexpr (PACK) {
+    // dsigma of each centre: its rows' sums in row order
+    if (threadIdx.x < 4 && sm.pk_cen[threadIdx.x] >= 0) {
+      float t = 0.f;
+      for (int k = sm.pk_off[threadIdx.x]; k < sm.pk_off[threadIdx.x + 1]; ++k) t += sm.rowpart[k];
+      sm.pk_dsig[threadIdx.x] = t;
+    }
+    __syncthreads();
+  } else {
+    for (int w = 0; w < nw; ++w) dsig += static_cast<float>(sm.red[8 + w]);
+  }
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    if constexpr (PACK) dsig = sm.pk_dsig[sm.rcen[j]];
     float dw = 0.f;
     float4 r = sm.dR[j];
     for (int w = 0; w < nw; ++w) {
@@ -590,16 +686,104 @@ __device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float
 }  // namespace
 
 size_t dp_scratch_floats(const DpArgs& a) {
-  const size_t nm = a.n_max, M2 = 2 * a.M, W = max_width(a);
+  const size_t nm = a.unit_rows, M2 = 2 * a.M, W = max_width(a);
   return align4(nm * M2) + nm * align4(nm) + align4(nm * W) * 2 + 64;
 }
 
 size_t dp_smem_bytes(const DpArgs& a, int mode) { return smem_layout(a, mode, nullptr, nullptr) + 1024; }
 
+// Descriptor of one centre from its rows [r0, r1) of the final features Xf (dp_core.hpp:
+// 358-384).  A = X^T R: thread per (feature m, k-half), all four R components at once,
+// coalesced over m; the two k-halves are added in a fixed order.  B = R^T X_< is the same
+// sums (B[q][r] = A[r][q] before scaling, product for product), so it is copied.  Writes
+// D[c], Ad[c], Bd[c]; ends with a barrier.
+__device__ void descriptor(const DpArgs& a, const float* Xf, int r0, int r1, int c, const Smem& sm) {
+  const int M = a.M, mr = a.mr;
+  {
+    float4* part = reinterpret_cast<float4*>(sm.head);  // [2][M]; operand stages idle
+    const int n = r1 - r0;
+    const int nh = (n + 1) >> 1;
+    const int half_threads = blockDim.x >> 1;
+    const int h = threadIdx.x / half_threads;
+    const int kb = r0 + h * nh, ke = min(r1, kb + nh);
+    for (int m = threadIdx.x - h * half_threads; m < M; m += half_threads) {
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+      for (int k = kb; k < ke; ++k) {
+        const float x = Xf[k * M + m];
+        const float4 R = sm.R[k];
+        a0 += x * R.x;
+        a1 += x * R.y;
+        a2 += x * R.z;
+        a3 += x * R.w;
+      }
+      part[h * M + m] = make_float4(a0, a1, a2, a3);
+    }
+    tc::fence_proxy_async();  // operand-stage memory: later overwritten by bulk copies
+    __syncthreads();
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+      const float4 p0 = part[m], p1 = part[M + m];
+      const float4 A = make_float4((p0.x + p1.x) * a.inv_sqrt_nmax, (p0.y + p1.y) * a.inv_sqrt_nmax,
+                                   (p0.z + p1.z) * a.inv_sqrt_nmax, (p0.w + p1.w) * a.inv_sqrt_nmax);
+      reinterpret_cast<float4*>(sm.Ad)[m] = A;
+      if (m < mr) {
+        sm.Bd[0 * mr + m] = A.x;
+        sm.Bd[1 * mr + m] = A.y;
+        sm.Bd[2 * mr + m] = A.z;
+        sm.Bd[3 * mr + m] = A.w;
+      }
+    }
+    __syncthreads();
+  }
+  float* D = a.D + static_cast<size_t>(c) * M * mr;
+  for (int idx = threadIdx.x; idx < M * mr; idx += blockDim.x) {
+    const int m = idx / mr, q = idx - m * mr;
+    float acc = 0.f;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) acc += sm.Ad[m * 4 + cc] * sm.Bd[cc * mr + q];
+    D[idx] = acc;
+  }
+  for (int idx = threadIdx.x; idx < M * 4; idx += blockDim.x) a.Ad[static_cast<size_t>(c) * M * 4 + idx] = sm.Ad[idx];
+  for (int idx = threadIdx.x; idx < 4 * mr; idx += blockDim.x) a.Bd[static_cast<size_t>(c) * 4 * mr + idx] = sm.Bd[idx];
+  __syncthreads();
+}
+
+// Row gradient g_k = de/dd_k of row k of centre c (dp_core.hpp:597-611) in FP64 geometry
+// from the env-row gradient dR_k and the switch-value gradient dsx_k; written to g[c][k].
+// w receives the row's virial products -g_a d_b.
+__device__ __forceinline__ void row_gradient(const DpArgs& a, int c, int k, float4 dr, float dsx, double (&w)[9]) {
+  const int cm = a.cen_member[c];
+  const int ca = a.m_atom[cm];
+  const int cs = a.m_shift[cm];
+  const int mj = a.nlist[static_cast<size_t>(c) * a.n_max + k];
+  const int aj = a.m_atom[mj];
+  const int sj = a.m_shift[mj];
+  const int rel[3] = {shift_x(sj) - shift_x(cs), shift_y(sj) - shift_y(cs), shift_z(sj) - shift_z(cs)};
+  double d[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) d[q] = image_delta(a.pos[3 * aj + q], a.pos[3 * ca + q], rel[q], a.L[q]);
+  const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
+  double s, ds;
+  switch_fn(r, a.rcs, a.rc, s, ds);
+  const double ir = 1.0 / r, sr = s * ir;
+  const double e[3] = {d[0] * ir, d[1] * ir, d[2] * ir};
+  const double dr0 = dr.x, dr1 = dr.y, dr2 = dr.z, dr3 = dr.w;
+  const double ge = dr1 * e[0] + dr2 * e[1] + dr3 * e[2];
+  const double coef = (dr0 + static_cast<double>(dsx)) * ds + (ds - sr) * ge;
+  const double gk[3] = {coef * e[0] + sr * dr1, coef * e[1] + sr * dr2, coef * e[2] + sr * dr3};
+  double* g = a.g + (static_cast<size_t>(c) * a.n_max + k) * 3;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    g[q] = gk[q];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) w[3 * q + b] = -gk[q] * d[b];
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // Forward: rows -> embedding -> attention layers -> descriptor D = (X^T R)(R^T X_<) / n_max
 // ------------------------------------------------------------------------------------
-template <int MODE, bool WIMG>
+template <int MODE, bool WIMG, bool PACK = false>
 __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant__ DpArgs a) {
   extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
@@ -618,23 +802,31 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
   }
 #endif
   const int M = a.M, M2 = 2 * M, mr = a.mr;
+  const int ur = a.unit_rows, ur4 = (ur + 3) & ~3;
+  const int n_units = PACK ? *a.n_units_dev : a.n_centres;
   CentreQueue queue(a.work);
-  for (int c = blockIdx.x; c < a.n_centres; c = queue.next()) {
-    const int n = a.nn[c];
+  // unit u: one centre (u = c), or a multi-centre pack (DpArgs::packs)
+  for (int u = blockIdx.x; u < n_units; u = queue.next()) {
+    int n, zi = 0;
+    float inv_sig = 0.f;
+    if constexpr (PACK) {
+      n = unit_rows_pack(a, u, sm);
+    } else {
+      n = a.nn[u];
+      const double sig = centre_rows(a, u, n, sm, zi);
+      inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
+    }
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
-    int zi;
-    const double sig = centre_rows(a, c, n, sm, zi);
     pc.mark(0);
-    const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
-    float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
-    embed_forward<MODE, WIMG>(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, X);
+    float* X = a.X + static_cast<size_t>(u) * ur * M;
+    embed_forward<MODE, WIMG, PACK>(mm, a, n, zi, sm, a.EMBst + static_cast<size_t>(u) * a.emb_centre_stride, X);
     pc.mark(1);
     for (int l = 0; l < a.n_attn; ++l) {
       const float* Xl = X + l * a.x_layer_stride;
       float* Xn = X + (l + 1) * a.x_layer_stride;
-      float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
-      float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
-      float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
+      float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(u) * ur * M2;
+      float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(u) * ur * ur4;
+      float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(u) * ur * ur4;
       mm.template run_wide<false, false, WIMG>(n, M2, M, Xl, M, a.ab[l], M2,
                                                 [&](int k, int j, auto v) { vst(&Ul[k * M2 + j], v); }, a.img_ab[l]);
       __syncthreads();
@@ -645,7 +837,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
           // S tile stays in shared memory: weighted softmax + gate fused into the epilogue
           mm.template run<false, true, 0, 2>(n, n, M, Ul, M2, Xl, M,
                                              [&](const float* stg, int ldst, int, int, int, int) {
-                                               softmax_gate(n, ln, stg, ldst, PUl, PTl, inv_sig, sm);
+                                               if constexpr (PACK) softmax_gate_rc<4, true>(n, ln, stg, ldst, PUl, PTl, inv_sig, sm);
+                                               else softmax_gate(n, ln, stg, ldst, PUl, PTl, inv_sig, sm);
                                              });
           pc.mark(3);
           fused_softmax = true;
@@ -669,57 +862,19 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
       __syncthreads();
       pc.mark(5);
     }
-    // descriptor (dp_core.hpp:358-384)
-    // A = X^T R: thread per (feature m, k-half), all four R components at once, coalesced
-    // over m; the two k-halves are added in a fixed order.  B = R^T X_< is the same sums
-    // (B[q][r] = A[r][q] before scaling, product for product), so it is copied.
+    // descriptor (dp_core.hpp:358-384), per centre of the unit over its rows
     const float* Xf = X + a.n_attn * a.x_layer_stride;
-    {
-      float4* part = reinterpret_cast<float4*>(sm.head);  // [2][M]; operand stages idle
-      const int nh = (n + 1) >> 1;
-      const int half_threads = blockDim.x >> 1;
-      const int h = threadIdx.x / half_threads;
-      const int kb = h * nh, ke = min(n, kb + nh);
-      for (int m = threadIdx.x - h * half_threads; m < M; m += half_threads) {
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 8
-        for (int k = kb; k < ke; ++k) {
-          const float x = Xf[k * M + m];
-          const float4 R = sm.R[k];
-          a0 += x * R.x;
-          a1 += x * R.y;
-          a2 += x * R.z;
-          a3 += x * R.w;
-        }
-        part[h * M + m] = make_float4(a0, a1, a2, a3);
+    const int n_cen = PACK ? 4 : 1;
+    for (int i = 0; i < n_cen; ++i) {
+      int c = u, r0 = 0, r1 = n;
+      if constexpr (PACK) {
+        c = sm.pk_cen[i];
+        if (c < 0) break;
+        r0 = sm.pk_off[i];
+        r1 = sm.pk_off[i + 1];
       }
-      tc::fence_proxy_async();  // operand-stage memory: later overwritten by bulk copies
-      __syncthreads();
-      for (int m = threadIdx.x; m < M; m += blockDim.x) {
-        const float4 p0 = part[m], p1 = part[M + m];
-        const float4 A = make_float4((p0.x + p1.x) * a.inv_sqrt_nmax, (p0.y + p1.y) * a.inv_sqrt_nmax,
-                                     (p0.z + p1.z) * a.inv_sqrt_nmax, (p0.w + p1.w) * a.inv_sqrt_nmax);
-        reinterpret_cast<float4*>(sm.Ad)[m] = A;
-        if (m < mr) {
-          sm.Bd[0 * mr + m] = A.x;
-          sm.Bd[1 * mr + m] = A.y;
-          sm.Bd[2 * mr + m] = A.z;
-          sm.Bd[3 * mr + m] = A.w;
-        }
-      }
-      __syncthreads();
+      descriptor(a, Xf, r0, r1, c, sm);
     }
-    float* D = a.D + static_cast<size_t>(c) * M * mr;
-    for (int idx = threadIdx.x; idx < M * mr; idx += blockDim.x) {
-      const int m = idx / mr, q = idx - m * mr;
-      float acc = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) acc += sm.Ad[m * 4 + cc] * sm.Bd[cc * mr + q];
-      D[idx] = acc;
-    }
-    for (int idx = threadIdx.x; idx < M * 4; idx += blockDim.x) a.Ad[static_cast<size_t>(c) * M * 4 + idx] = sm.Ad[idx];
-    for (int idx = threadIdx.x; idx < 4 * mr; idx += blockDim.x) a.Bd[static_cast<size_t>(c) * 4 * mr + idx] = sm.Bd[idx];
-    __syncthreads();
     pc.mark(6);
   }
   pc.flush();
@@ -730,7 +885,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
 // Backward: dD -> (dA, dB) -> dX, dR -> attention layers in reverse -> embedding ->
 // row gradients g_k = de/dd_k (FP64 geometry), per-centre virial -sum g (x) d.
 // ------------------------------------------------------------------------------------
-template <int MODE, bool WIMG>
+template <int MODE, bool WIMG, bool PACK = false>
 __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constant__ DpArgs a) {
   extern __shared__ __align__(1024) unsigned char dp_smem_raw[];
   unsigned char* dp_smem = dp_smem_raw + ((1024 - (tc::smem_u32(dp_smem_raw) & 1023)) & 1023);
@@ -750,104 +905,124 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
 #endif
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ur = a.unit_rows, ur4 = (ur + 3) & ~3;
+  const int n_units = PACK ? *a.n_units_dev : a.n_centres;
   CentreQueue queue(a.work);
-  for (int c = blockIdx.x; c < a.n_centres; c = queue.next()) {
-    const int n = a.nn[c];
+  // unit u: one centre (u = c), or a multi-centre pack (DpArgs::packs)
+  for (int u = blockIdx.x; u < n_units; u = queue.next()) {
+    int n, zi = 0;
+    float inv_sig = 0.f;
+    if constexpr (PACK) {
+      n = unit_rows_pack(a, u, sm);
+    } else {
+      n = a.nn[u];
+      const double sig = centre_rows(a, u, n, sm, zi);
+      inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
+    }
+    (void)zi;
     const int ln = (n + 3) & ~3;  // leading dimension of the n x n scratch matrices
     const Slot sl = slot_of(a, a.scratch + static_cast<size_t>(blockIdx.x) * a.scratch_slot, n);
-    int zi;
-    const double sig = centre_rows(a, c, n, sm, zi);
     pc.mark(0);
-    const float inv_sig = sig > 0.0 ? static_cast<float>(1.0 / sig) : 0.f;
-    const float* X = a.X + static_cast<size_t>(c) * a.n_max * M;
+    const float* X = a.X + static_cast<size_t>(u) * ur * M;
     const float* Xf = X + a.n_attn * a.x_layer_stride;
-    const float* dD = a.dD + static_cast<size_t>(c) * M * mr;
-    const float* Ad = a.Ad + static_cast<size_t>(c) * M * 4;
-    const float* Bd = a.Bd + static_cast<size_t>(c) * 4 * mr;
     if (threadIdx.x == 0 && !(a.flags & 1)) {
       // forward stash read first: final features (dR below) and the top layer's U
       prefetch_l2(Xf, sizeof(float) * n * M);
       if (a.n_attn > 0)
-        prefetch_l2(a.Ust + (a.n_attn - 1) * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2,
+        prefetch_l2(a.Ust + (a.n_attn - 1) * a.u_layer_stride + static_cast<size_t>(u) * ur * M2,
                     sizeof(float) * n * M2);
     }
-    // dA[m][cc] = sum_q dD[m,q] B[cc,q];  dB[cc][q] = sum_m dD[m,q] A[m,cc]
-    // (operands staged into shared memory with coalesced loads; the tensor-core stage
-    // buffers are idle between GEMMs)
-    {
-      const float* sdD = dD;
-      const float* sAd = Ad;
-      const float* sBd = Bd;
-      if constexpr (MODE != 0) {
-        float* tmp = reinterpret_cast<float*>(sm.head);
-        if (((M * mr) & 3) == 0) {
-          for (int i = threadIdx.x; i < (M * mr) >> 2; i += blockDim.x)
-            reinterpret_cast<float4*>(tmp)[i] = reinterpret_cast<const float4*>(dD)[i];
-        } else {
-          for (int i = threadIdx.x; i < M * mr; i += blockDim.x) tmp[i] = dD[i];
-        }
-        for (int i = threadIdx.x; i < M * 4; i += blockDim.x) tmp[M * mr + i] = Ad[i];
-        for (int i = threadIdx.x; i < 4 * mr; i += blockDim.x) tmp[M * mr + M * 4 + i] = Bd[i];
-        tc::fence_proxy_async();  // operand-stage memory: later overwritten by bulk copies
-        __syncthreads();
-        sdD = tmp;
-        sAd = tmp + M * mr;
-        sBd = tmp + M * mr + M * 4;
-      }
-      for (int idx = threadIdx.x; idx < M * 4 + 4 * mr; idx += blockDim.x) {
-        float acc = 0.f;
-        if (idx < M * 4) {
-          const int m = idx >> 2, cc = idx & 3;
-          for (int q = 0; q < mr; ++q) acc += sdD[m * mr + q] * sBd[cc * mr + q];
-          sm.dAd[idx] = acc;
-        } else {
-          const int j = idx - M * 4, cc = j / mr, q = j - cc * mr;
-          for (int m = 0; m < M; ++m) acc += sdD[m * mr + q] * sAd[m * 4 + cc];
-          sm.dBd[j] = acc;
-        }
-      }
-      for (int k = threadIdx.x; k < n; k += blockDim.x) sm.dsx[k] = 0.f;
-      __syncthreads();
-    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) sm.dsx[k] = 0.f;
     float* dY = sl.DX0;
     float* dXn = sl.DX1;
     const float inm = a.inv_sqrt_nmax;
-    for (int idx = threadIdx.x; idx < n * M; idx += blockDim.x) {
-      const int k = idx / M, m = idx - k * M;
-      const float* R = reinterpret_cast<const float*>(&sm.R[k]);
-      const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];  // one conflict-free 16-byte read
-      float v = da.x * R[0];
-      v += da.y * R[1];
-      v += da.z * R[2];
-      v += da.w * R[3];
-      if (m < mr)
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) v += sm.dBd[cc * mr + m] * R[cc];
-      dY[idx] = v * inm;
-    }
-    // dR_k = (X_k dA + X_k[:mr] dB^T) / sqrt(n_max): warp per row, lanes over features
-    for (int k = wid; k < n; k += nw) {
-      float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
-#pragma unroll 4
-      for (int m = lane; m < M; m += 32) {
-        const float x = Xf[k * M + m];
-        const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];
-        v0 += x * da.x;
-        v1 += x * da.y;
-        v2 += x * da.z;
-        v3 += x * da.w;
-        if (m < mr) {
-          v0 += x * sm.dBd[0 * mr + m];
-          v1 += x * sm.dBd[1 * mr + m];
-          v2 += x * sm.dBd[2 * mr + m];
-          v3 += x * sm.dBd[3 * mr + m];
-        }
+    const int n_cen = PACK ? 4 : 1;
+    for (int i = 0; i < n_cen; ++i) {
+      int c = u, r0 = 0, r1 = n;
+      if constexpr (PACK) {
+        c = sm.pk_cen[i];
+        if (c < 0) break;
+        r0 = sm.pk_off[i];
+        r1 = sm.pk_off[i + 1];
       }
-      v0 = warp_sum(v0);
-      v1 = warp_sum(v1);
-      v2 = warp_sum(v2);
-      v3 = warp_sum(v3);
-      if (lane == 0) sm.dR[k] = make_float4(v0 * inm, v1 * inm, v2 * inm, v3 * inm);
+      const float* dD = a.dD + static_cast<size_t>(c) * M * mr;
+      const float* Ad = a.Ad + static_cast<size_t>(c) * M * 4;
+      const float* Bd = a.Bd + static_cast<size_t>(c) * 4 * mr;
+      // dA[m][cc] = sum_q dD[m,q] B[cc,q];  dB[cc][q] = sum_m dD[m,q] A[m,cc]
+      // (operands staged into shared memory with coalesced loads; the tensor-core stage
+      // buffers are idle between GEMMs)
+      {
+        const float* sdD = dD;
+        const float* sAd = Ad;
+        const float* sBd = Bd;
+        if constexpr (MODE != 0) {
+          float* tmp = reinterpret_cast<float*>(sm.head);
+          if (((M * mr) & 3) == 0) {
+            for (int i2 = threadIdx.x; i2 < (M * mr) >> 2; i2 += blockDim.x)
+              reinterpret_cast<float4*>(tmp)[i2] = reinterpret_cast<const float4*>(dD)[i2];
+          } else {
+            for (int i2 = threadIdx.x; i2 < M * mr; i2 += blockDim.x) tmp[i2] = dD[i2];
+          }
+          for (int i2 = threadIdx.x; i2 < M * 4; i2 += blockDim.x) tmp[M * mr + i2] = Ad[i2];
+          for (int i2 = threadIdx.x; i2 < 4 * mr; i2 += blockDim.x) tmp[M * mr + M * 4 + i2] = Bd[i2];
+          tc::fence_proxy_async();  // operand-stage memory: later overwritten by bulk copies
+          __syncthreads();
+          sdD = tmp;
+          sAd = tmp + M * mr;
+          sBd = tmp + M * mr + M * 4;
+        }
+        for (int idx = threadIdx.x; idx < M * 4 + 4 * mr; idx += blockDim.x) {
+          float acc = 0.f;
+          if (idx < M * 4) {
+            const int m = idx >> 2, cc = idx & 3;
+            for (int q = 0; q < mr; ++q) acc += sdD[m * mr + q] * sBd[cc * mr + q];
+            sm.dAd[idx] = acc;
+          } else {
+            const int j = idx - M * 4, cc = j / mr, q = j - cc * mr;
+            for (int m = 0; m < M; ++m) acc += sdD[m * mr + q] * sAd[m * 4 + cc];
+            sm.dBd[j] = acc;
+          }
+        }
+        __syncthreads();
+      }
+      for (int idx = r0 * M + threadIdx.x; idx < r1 * M; idx += blockDim.x) {
+        const int k = idx / M, m = idx - k * M;
+        const float* R = reinterpret_cast<const float*>(&sm.R[k]);
+        const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];  // one conflict-free 16-byte read
+        float v = da.x * R[0];
+        v += da.y * R[1];
+        v += da.z * R[2];
+        v += da.w * R[3];
+        if (m < mr)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) v += sm.dBd[cc * mr + m] * R[cc];
+        dY[idx] = v * inm;
+      }
+      // dR_k = (X_k dA + X_k[:mr] dB^T) / sqrt(n_max): warp per row, lanes over features
+      for (int k = r0 + wid; k < r1; k += nw) {
+        float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
+#pragma unroll 4
+        for (int m = lane; m < M; m += 32) {
+          const float x = Xf[k * M + m];
+          const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];
+          v0 += x * da.x;
+          v1 += x * da.y;
+          v2 += x * da.z;
+          v3 += x * da.w;
+          if (m < mr) {
+            v0 += x * sm.dBd[0 * mr + m];
+            v1 += x * sm.dBd[1 * mr + m];
+            v2 += x * sm.dBd[2 * mr + m];
+            v3 += x * sm.dBd[3 * mr + m];
+          }
+        }
+        v0 = warp_sum(v0);
+        v1 = warp_sum(v1);
+        v2 = warp_sum(v2);
+        v3 = warp_sum(v3);
+        if (lane == 0) sm.dR[k] = make_float4(v0 * inm, v1 * inm, v2 * inm, v3 * inm);
+      }
+      if constexpr (PACK) __syncthreads();  // dAd / dBd are reused by the unit's next centre
     }
     __syncthreads();
     pc.mark(1);
@@ -855,9 +1030,9 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       const float* Xl = X + l * a.x_layer_stride;
       const float* AB = a.ab[l];
       // forward stash: U = X [A|B], pu, P~ of this layer (no recompute)
-      const float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(c) * a.n_max * M2;
-      const float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
-      const float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(c) * a.n_max * ((a.n_max + 3) & ~3);
+      const float* Ul = a.Ust + l * a.u_layer_stride + static_cast<size_t>(u) * ur * M2;
+      const float* PUl = a.PUst + l * a.p_layer_stride + static_cast<size_t>(u) * ur * ur4;
+      const float* PTl = a.PTst + l * a.p_layer_stride + static_cast<size_t>(u) * ur * ur4;
       if (threadIdx.x == 0 && !(a.flags & 1)) {
         // this layer's stash and the next (lower) layer's U are read from HBM below:
         // start pulling them into L2 now
@@ -865,7 +1040,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         prefetch_l2(PTl, sizeof(float) * n * ln);
         prefetch_l2(Xl, sizeof(float) * n * M);
         if (l > 0) prefetch_l2(Ul - a.u_layer_stride, sizeof(float) * n * M2);
-        else prefetch_l2(a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride, sizeof(float) * a.emb_centre_stride);
+        else prefetch_l2(a.EMBst + static_cast<size_t>(u) * a.emb_centre_stride, sizeof(float) * a.emb_centre_stride);
       }
       pc.mark(2);
       // T = dP~ = dY U_B^T, then the row and column passes (bwd_row_pass, bwd_col_pass)
@@ -875,16 +1050,16 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       // same (idle) operand-stage buffer.
       bool fused_rc = false;
       if constexpr (MODE != 0) {
-        if (n <= 128 && !(a.flags & 2)) {
+        if (PACK || (n <= 128 && !(a.flags & 2))) {
           unsigned char* part = sm.head + kPartOff;
           mm.template run<false, true, 0, 2>(n, n, M, dY, M, Ul + M, M2,
                                              [&](const float* stg, int ldst, int, int, int, int) {
-                                               bwd_rc_pass(n, ln, stg, ldst, PUl, sl.T, inv_sig, sm, part);
+                                               bwd_rc_pass<PACK>(n, ln, stg, ldst, PUl, sl.T, inv_sig, sm, part);
                                              });
           fused_rc = true;
         }
       }
-      if (!fused_rc) {
+      if (!PACK && !fused_rc) {
         mm.template run<false, true>(n, n, M, dY, M, Ul + M, M2,
                                      [&](int k, int j, auto v) { vst(&sl.T[k * ln + j], v); });
         __syncthreads();
@@ -943,11 +1118,11 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       size_t off = 0;
       for (int e = 0; e + 1 < a.n_embed; ++e) {
         offs[e] = off;
-        off += static_cast<size_t>(a.n_max) * a.edims[e];
+        off += static_cast<size_t>(ur) * a.edims[e];
       }
       for (int e = a.n_embed - 1; e >= 1; --e) {
         const int Ein = a.edims[e - 1], Eout = a.edims[e];
-        const float* __restrict__ h = a.EMBst + static_cast<size_t>(c) * a.emb_centre_stride + offs[e - 1];
+        const float* __restrict__ h = a.EMBst + static_cast<size_t>(u) * a.emb_centre_stride + offs[e - 1];
         float* __restrict__ xo = dXn;
         mm.template run<false, false, 0, 1, WIMG>(n, Ein, Eout, dY, Eout, a.ew[e], Ein,
                                                   [=](int k, int i, auto v) {
@@ -983,37 +1158,38 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
     }
     pc.mark(12);
     // row gradients (dp_core.hpp:597-611) in FP64 geometry; virial W_ab -= g_a d_b
-    {
-      const int cm = a.cen_member[c];
-      const int ca = a.m_atom[cm];
-      const int cs = a.m_shift[cm];
-      const int* list = a.nlist + static_cast<size_t>(c) * a.n_max;
-      double* g = a.g + static_cast<size_t>(c) * a.n_max * 3;
+    if constexpr (PACK) {
+      // rows of several centres (one row per thread, n <= 128): each row's nine products in
+      // shared memory (the operand stage is idle), then per centre a fixed-order row sum
+      double* wrow = reinterpret_cast<double*>(sm.head);  // [n][9]
+      const int k = threadIdx.x;
+      if (k < n) {
+        const int i = sm.rcen[k];
+        const int c = sm.pk_cen[i], kk = k - sm.pk_off[i];
+        double w[9];
+        row_gradient(a, c, kk, sm.dR[k], sm.dsx[k], w);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) wrow[9 * k + q] = w[q];
+      }
+      __syncthreads();
+      if (threadIdx.x < 36) {
+        const int i = threadIdx.x / 9, q = threadIdx.x - 9 * i;
+        const int c = sm.pk_cen[i];
+        if (c >= 0) {
+          double t = 0.0;  // row order: deterministic
+          for (int r = sm.pk_off[i]; r < sm.pk_off[i + 1]; ++r) t += wrow[9 * r + q];
+          a.vir[static_cast<size_t>(c) * 9 + q] = t;
+        }
+      }
+      tc::fence_proxy_async();  // operand stage: later overwritten by bulk copies
+    } else {
+      const int c = u;
       double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
       for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        const int mj = list[k];
-        const int aj = a.m_atom[mj];
-        const int sj = a.m_shift[mj];
-        const int rel[3] = {shift_x(sj) - shift_x(cs), shift_y(sj) - shift_y(cs), shift_z(sj) - shift_z(cs)};
-        double d[3];
+        double wk[9];
+        row_gradient(a, c, k, sm.dR[k], sm.dsx[k], wk);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) d[q] = image_delta(a.pos[3 * aj + q], a.pos[3 * ca + q], rel[q], a.L[q]);
-        const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
-        double s, ds;
-        switch_fn(r, a.rcs, a.rc, s, ds);
-        const double ir = 1.0 / r, sr = s * ir;
-        const double e[3] = {d[0] * ir, d[1] * ir, d[2] * ir};
-        const float4 dr = sm.dR[k];
-        const double dr0 = dr.x, dr1 = dr.y, dr2 = dr.z, dr3 = dr.w;
-        const double ge = dr1 * e[0] + dr2 * e[1] + dr3 * e[2];
-        const double coef = (dr0 + static_cast<double>(sm.dsx[k])) * ds + (ds - sr) * ge;
-        const double gk[3] = {coef * e[0] + sr * dr1, coef * e[1] + sr * dr2, coef * e[2] + sr * dr3};
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          g[3 * k + q] = gk[q];
-#pragma unroll
-          for (int b = 0; b < 3; ++b) w[3 * q + b] -= gk[q] * d[b];
-        }
+        for (int q = 0; q < 9; ++q) w[q] += wk[q];
       }
       // the nine sums with one barrier: warp sums, then a fixed-order sum over warps
       // (block_sum's order, so the same bits), parked in dA's (dead) shared buffer
@@ -1080,10 +1256,10 @@ void launch_weight_image(const float* W, int TB, int ldb, int K, int N, uint8_t*
 }
 
 
-template <int MODE, bool WIMG>
+template <int MODE, bool WIMG, bool PACK>
 static void set_smem(size_t smem) {
-  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_forward<MODE, WIMG>), smem);
-  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_backward<MODE, WIMG>), smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_forward<MODE, WIMG, PACK>), smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(k_centre_backward<MODE, WIMG, PACK>), smem);
 }
 
 template <bool FWD>
@@ -1091,20 +1267,24 @@ static void launch_centre(const DpArgs& a, int grid, cudaStream_t st) {
   if (a.n_centres == 0) return;
   cudaMemsetAsync(a.work, 0, sizeof(int), st);
   const size_t smem = dp_smem_bytes(a, a.mode);
-  auto go = [&](auto mode_c, auto wimg_c) {
+  auto go = [&](auto mode_c, auto wimg_c, auto pack_c) {
     constexpr int MODE = decltype(mode_c)::value;
     constexpr bool WIMG = decltype(wimg_c)::value;
-    set_smem<MODE, WIMG>(smem);
-    if (FWD) k_centre_forward<MODE, WIMG><<<grid, 256, smem, st>>>(a);
-    else k_centre_backward<MODE, WIMG><<<grid, 256, smem, st>>>(a);
+    constexpr bool PACK = decltype(pack_c)::value;
+    set_smem<MODE, WIMG, PACK>(smem);
+    if (FWD) k_centre_forward<MODE, WIMG, PACK><<<grid, 256, smem, st>>>(a);
+    else k_centre_backward<MODE, WIMG, PACK><<<grid, 256, smem, st>>>(a);
   };
   using T = std::true_type;
   using F = std::false_type;
-  if (a.mode == 0) go(std::integral_constant<int, 0>{}, F{});
-  else if (a.mode == 1 && a.wimg) go(std::integral_constant<int, 1>{}, T{});
-  else if (a.mode == 1) go(std::integral_constant<int, 1>{}, F{});
-  else if (a.wimg) go(std::integral_constant<int, 2>{}, T{});
-  else go(std::integral_constant<int, 2>{}, F{});
+  // multi-centre units only with tcgen05 and weight images (context.cpp decides)
+  if (a.packs && a.mode == 1) go(std::integral_constant<int, 1>{}, T{}, T{});
+  else if (a.packs) go(std::integral_constant<int, 2>{}, T{}, T{});
+  else if (a.mode == 0) go(std::integral_constant<int, 0>{}, F{}, F{});
+  else if (a.mode == 1 && a.wimg) go(std::integral_constant<int, 1>{}, T{}, F{});
+  else if (a.mode == 1) go(std::integral_constant<int, 1>{}, F{}, F{});
+  else if (a.wimg) go(std::integral_constant<int, 2>{}, T{}, F{});
+  else go(std::integral_constant<int, 2>{}, F{}, F{});
   count_launch();
 }
 

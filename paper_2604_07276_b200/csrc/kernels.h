@@ -239,7 +239,20 @@ struct DpArgs {
   const uint8_t* img_ewT[kMaxLayers];
   int wimg;  // 1: all of the above are present (the per-centre kernels' WIMG variant)
   int* work;  // dynamic centre counter of the persistent per-centre kernels (zeroed per launch)
+  // Work units of the per-centre kernels.  packs == NULL: one centre per unit (unit u =
+  // centre u, unit_rows = n_max).  Otherwise (n_max <= 64, tcgen05 modes) consecutive centres
+  // share one 128-row tile: packs[u] = (first centre, centre count <= 4), *n_units_dev units,
+  // unit_rows = 128; the n x n matrices of a unit are block diagonal (one block per centre).
+  // The stash (X, U, pu, P~, embedding activations) is indexed by unit with unit_rows rows.
+  const int2* packs;
+  const int* n_units_dev;
+  int unit_rows;
 };
+// Packs of consecutive centres (groups of 4: one pack if their rows fit 128, else two
+// pairs); units written to packs, their count to *n_units.  cnt/off: scratch of
+// ceil(n_centres/4) + 1 ints.
+void launch_pack_plan(const int* nn, int n_centres, int* cnt, int* off, int2* packs, cudaStream_t st);
+inline int pack_capacity(int n_centres) { return 2 * ((n_centres + 3) / 4); }
 // Weight images: bytes for a K x N operand, and the builder (B(k,n) = TB ? W[n*ldb+k] :
 // W[k*ldb+n]).
 size_t weight_image_bytes(int K, int N);

@@ -265,7 +265,13 @@ def test_paper_model_cutoff_sweep_spotcheck(rc):
     m = nb.init_model(nb.paper_spec(rc), 1)
     r1 = nb.DeviceEvaluator(m, n_ranks=1).compute(pos, sp, box)
     r8 = nb.DeviceEvaluator(m, n_ranks=8 if rc == 4.0 else 1).compute(pos, sp, box)
-    assert np.array_equal(r1["atom_energy"], r8["atom_energy"])
+    if rc == 4.0:
+        # n_max 64: centres run as multi-centre 128-row units whose composition follows the
+        # rank's centre order, so FP32 accumulation order (not the arithmetic) varies with
+        # the rank count
+        assert rel_err(r8["atom_energy"], r1["atom_energy"]) <= 1e-6
+    else:
+        assert np.array_equal(r1["atom_energy"], r8["atom_energy"])
     port = O.Port()
     h = port.model_init(dict(O.PAPER_SPEC, rc=rc, rcs=0.55 * rc, n_max=O.nmax_for_rc(rc)), 1)
     counts, mem, img, d = port.neighbor_rows(h, pos, sp, box)
@@ -276,3 +282,18 @@ def test_paper_model_cutoff_sweep_spotcheck(rc):
         assert abs(r1["atom_energy"][c] - e) <= 1e-5 * max(abs(e), 1e-2), (c, r1["atom_energy"][c], e)
     port.model_free(h)
 
+
+
+def test_multi_centre_units_match_single_centre_path(monkeypatch):
+    """rc = 4 (n_max 64): multi-centre 128-row units (up to four centres per tile, block-
+    diagonal attention) against the one-centre-per-tile path (NNMD_FLAGS bit 3) on the
+    same inputs: energies, forces, virial and per-atom energies within 1e-6, rows equal."""
+    box, pos, sp = nb.synth_system(1200, 0.1, 0.9, 9)
+    m = nb.init_model(nb.paper_spec(4.0), 3)
+    monkeypatch.setenv("NNMD_FLAGS", "8")
+    single = nb.DeviceEvaluator(m, n_ranks=2).compute(pos, sp, box)
+    monkeypatch.delenv("NNMD_FLAGS")
+    packed = nb.DeviceEvaluator(m, n_ranks=2).compute(pos, sp, box)
+    assert abs(packed["energy"] - single["energy"]) <= 1e-6 * abs(single["energy"])
+    for k in ("forces", "virial", "atom_energy"):
+        assert rel_err(packed[k], single[k]) <= 1e-6, k
