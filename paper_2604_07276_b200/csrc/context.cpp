@@ -738,6 +738,9 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   fa.e = e_.p;
   fa.dD = dD_.p;
   fa.mode = dp.mode;
+  fa.n_sm = n_sm_;
+  fitws_.ensure(fit_workspace_floats(ncen, 256, n_sm_));  // split-K only for layers with N <= 256
+  fa.ws = fitws_.p;
   tic("fit");
   launch_fit(fa, st_);
   toc();

@@ -149,7 +149,7 @@ class Context {
   DevBuf<int> cs_i_;         // cell-ordered packed shift | species
   DevBuf<int64_t> cs_gid_;   // cell-ordered gids
   DevBuf<int> nlist_, nn_, rlist_, rn_, maxn_, work_;
-  DevBuf<float> X_, Ad_, Bd_, D_, dD_, scratch_, fitY_, fitd_, Ust_, PUst_, PTst_, EMBst_;
+  DevBuf<float> X_, Ad_, Bd_, D_, dD_, scratch_, fitY_, fitd_, fitws_, Ust_, PUst_, PTst_, EMBst_;
   DevBuf<float4> R_;
   DevBuf<double> g_, vir_, e_, fmem_, sig_;
   DevBuf<int> Z_;

@@ -1296,7 +1296,18 @@ void launch_centre_backward(const DpArgs& a, int grid, cudaStream_t st) { launch
 // ------------------------------------------------------------------------------------
 enum { EPI_STORE = 0, EPI_TANH_BIAS = 1, EPI_DTANH = 2 };
 
-// One output tile per CTA: SIMT 64x64 (MODE 0) or tcgen05 128x256 (MODE 1/2).
+// Split-K (tcgen05 modes): CTA z of gridDim.z takes K range [z Kc, (z+1) Kc) (Kc a multiple
+// of the 128-wide FP32 promotion group) and stores its raw tile to the workspace slice z;
+// k_fit_splitk_sum then adds the slices in slice order and applies the epilogue.  The
+// split depends on K only, never on the centre count, so a centre's energy is the same
+// bits at every DD rank count; it matters when few row tiles (many ranks) leave SMs idle
+// over the K = M * mr = 4096 reduction.
+constexpr int kFitSplit = 8;
+
+__host__ __device__ inline int fit_split(int K) {
+  return (K >= 1024 && (K / 128) % kFitSplit == 0) ? kFitSplit : 1;
+}
+
 template <bool TB, int MODE>
 __global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const float* __restrict__ A,
                                                      const float* __restrict__ B, int ldb,
@@ -1308,36 +1319,62 @@ __global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const 
   constexpr int TN = MODE == 0 ? kTN : tc::kNT;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int Ms = min(TM, M - m0), Ns = min(TN, N - n0);
-  const float* Ab = A + static_cast<size_t>(m0) * K;
-  const float* Bb = TB ? B + static_cast<size_t>(n0) * ldb : B + n0;
+  // split-K slice (gridDim.z > 1): raw partial tile into C's slice z, epilogue later
+  const int Kc = K / static_cast<int>(gridDim.z), kz = static_cast<int>(blockIdx.z) * Kc;
+  const float* Ab = A + static_cast<size_t>(m0) * K + kz;
+  const float* Bb = (TB ? B + static_cast<size_t>(n0) * ldb : B + n0) + (TB ? kz : static_cast<size_t>(kz) * ldb);
+  float* Cz = C + static_cast<size_t>(blockIdx.z) * M * N;
+  const int mode = gridDim.z > 1 ? EPI_STORE : epi_mode;
   Mm<MODE, 2> mm;
   mm.init(head, 512);
-  mm.template run<false, TB, 4>(Ms, Ns, K, Ab, K, Bb, ldb, [&](int m, int n, auto v) {
+  mm.template run<false, TB, 4>(Ms, Ns, Kc, Ab, K, Bb, ldb, [&](int m, int n, auto v) {
     const size_t o = static_cast<size_t>(m0 + m) * N + n0 + n;
-    if (epi_mode == EPI_TANH_BIAS) v = vtanh(v + vld(&bias[n0 + n], v));
-    else if (epi_mode == EPI_DTANH) v = v * vdtanh(vld(&Y[o], v));
-    vst(&C[o], v);
+    if (mode == EPI_TANH_BIAS) v = vtanh(v + vld(&bias[n0 + n], v));
+    else if (mode == EPI_DTANH) v = v * vdtanh(vld(&Y[o], v));
+    vst(&Cz[o], v);
   });
   mm.finish();
 }
 
+__global__ void k_fit_splitk_sum(int M, int N, int S, const float* __restrict__ P, float* __restrict__ C,
+                                 const float* __restrict__ bias, const float* __restrict__ Y, int epi_mode) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const size_t MN = static_cast<size_t>(M) * N;
+  if (i >= MN) return;
+  float v = P[i];
+  for (int z = 1; z < S; ++z) v += P[z * MN + i];
+  if (epi_mode == EPI_TANH_BIAS) v = tanhf(v + bias[i % N]);
+  else if (epi_mode == EPI_DTANH) v = v * (1.f - Y[i] * Y[i]);
+  C[i] = v;
+}
+
 template <bool TB, int MODE>
 static void fit_gemm(int M, int N, int K, const float* A, const float* B, int ldb, float* C, const float* bias,
-                     const float* Y, int epi, cudaStream_t st) {
+                     const float* Y, int epi, cudaStream_t st, float* ws = nullptr, int n_sm = 0) {
   constexpr int TM = MODE == 0 ? kTM : tc::kMT;
   constexpr int TN = MODE == 0 ? kTN : tc::kNT;
   const size_t smem = head_bytes(MODE, 2) + 1024;
   ensure_smem_attr(reinterpret_cast<const void*>(k_fit_gemm<TB, MODE>), smem);
-  dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM);
-  k_fit_gemm<TB, MODE><<<grid, 256, smem, st>>>(M, N, K, A, B, ldb, C, bias, Y, epi);
+  const int S = (MODE != 0 && ws && N <= TN) ? fit_split(K) : 1;
+  dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, S);
+  k_fit_gemm<TB, MODE><<<grid, 256, smem, st>>>(M, N, K, A, B, ldb, S > 1 ? ws : C, bias, Y, epi);
   count_launch();
+  if (S > 1) {
+    const size_t MN = static_cast<size_t>(M) * N;
+    k_fit_splitk_sum<<<static_cast<int>((MN + 255) / 256), 256, 0, st>>>(M, N, S, ws, C, bias, Y, epi);
+    count_launch();
+  }
 }
 
 template <int MODE>
 static void fit_gemm_tb(bool tb, int M, int N, int K, const float* A, const float* B, int ldb, float* C,
-                        const float* bias, const float* Y, int epi, cudaStream_t st) {
-  if (tb) fit_gemm<true, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st);
-  else fit_gemm<false, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st);
+                        const float* bias, const float* Y, int epi, cudaStream_t st, float* ws, int n_sm) {
+  if (tb) fit_gemm<true, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st, ws, n_sm);
+  else fit_gemm<false, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st, ws, n_sm);
+}
+
+size_t fit_workspace_floats(int n_centres, int width, int) {
+  return static_cast<size_t>(kFitSplit) * n_centres * width + 4;
 }
 
 // e[c] = b + w . Y[c]   (linear output layer); delta[c][o] = w[o] (1 - Y[c][o]^2)
@@ -1369,9 +1406,9 @@ void launch_fit(const FitArgs& a, cudaStream_t st) {
   const int L = a.n_fit;
   auto gemm = [&](bool tb, int N, int K, const float* A, const float* B, int ldb, float* C,
                   const float* bias, const float* Y, int mode) {
-    if (a.mode == 0) fit_gemm_tb<0>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st);
-    else if (a.mode == 1) fit_gemm_tb<1>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st);
-    else fit_gemm_tb<2>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st);
+    if (a.mode == 0) fit_gemm_tb<0>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st, nullptr, 0);
+    else if (a.mode == 1) fit_gemm_tb<1>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st, a.ws, a.n_sm);
+    else fit_gemm_tb<2>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st, a.ws, a.n_sm);
   };
   // forward hidden layers: Y_l = tanh(X W_l^T + b_l)
   const float* x = a.D;

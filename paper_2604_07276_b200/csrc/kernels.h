@@ -278,7 +278,12 @@ struct FitArgs {
   double* e;                 // [n_centres]
   float* dD;
   int mode;
+  int n_sm;                  // SMs of the device (split-K sizing)
+  float* ws;                 // split-K partial sums, fit_workspace_floats(...) floats
 };
+// Split-K workspace of the fitting net's K = M * mr layer (small centre counts: one row
+// tile per 128 centres cannot fill the GPU, so K is split and the partials summed in order)
+size_t fit_workspace_floats(int n_centres, int width, int n_sm);
 void launch_fit(const FitArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- MD loop -------------
