@@ -354,7 +354,13 @@ __device__ void softmax_gate_rc(int n, int ln, const float* S, int lds, float* P
     Rj[t] = j < n ? sm.R[j] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (int k = wid; k < n; k += nw) {
-    const float* row = S + static_cast<size_t>(k) * lds;
+    // the row's scores, all loads issued before the reductions
+    float cur[C];
+#pragma unroll
+    for (int t = 0; t < C; ++t) {
+      const int j = lane + 32 * t;
+      cur[t] = j < n ? S[static_cast<size_t>(k) * lds + j] : 0.f;
+    }
     int jb = 0, je = n;
     if constexpr (PACK) {
       const int i = sm.rcen[k];
@@ -367,7 +373,7 @@ __device__ void softmax_gate_rc(int n, int ln, const float* S, int lds, float* P
 #pragma unroll
     for (int t = 0; t < C; ++t) {
       const int j = lane + 32 * t;
-      e[t] = (j >= jb && j < je) ? row[j] : -FLT_MAX;
+      e[t] = (j >= jb && j < je) ? cur[t] : -FLT_MAX;
       mx = fmaxf(mx, e[t]);
     }
     mx = warp_max(mx);
@@ -539,6 +545,91 @@ __device__ void bwd_col_pass(int n, int ln, int stride, const float* TS, int ldt
     sm.dR[j] = r;
   }
   tc::fence_proxy_async();  // part may sit in an operand stage that bulk copies overwrite later
+}
+
+// Column pass for any n, after bwd_row_pass (t_k, the dsigma row partials, the row gate
+// term): columns in windows of 128, warp per query row k, lane owning 4 columns of the
+// window (coalesced 16-byte loads of dP~ and pu, 16-byte dS stores), the column sums dw_j
+// and sum_k dC_kj R_k kept in registers across the warp's rows and reduced over warps
+// once per window.  Same quantities as bwd_col_pass; DS may alias TS (ldt == ln).
+// part: [nw][128] float4 + [nw][128] float of shared memory.
+__device__ void bwd_colwin_pass(int n, int ln, const float* TS, int ldt, const float* __restrict__ PU, float* DS,
+                                float inv_sig, const Smem& sm, unsigned char* part_raw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float4* pg = reinterpret_cast<float4*>(part_raw);     // [nw][128]
+  float* pw = reinterpret_cast<float*>(pg + nw * 128);  // [nw][128]
+  if (threadIdx.x == blockDim.x - 1) {
+    float ds = 0.f;
+    for (int k = 0; k < n; ++k) ds += sm.rowpart[k];
+    sm.red[0] = ds;
+  }
+  for (int c0 = 0; c0 < n; c0 += 128) {
+    const int j4 = c0 + 4 * lane;
+    const bool act = j4 < n;
+    float sj2[4];
+    float4 Rj[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool v = j4 + q < n;
+      const float sj = v ? sm.s[j4 + q] : 0.f;
+      sj2[q] = sj * sj;
+      Rj[q] = v ? sm.R[j4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float cw[4] = {0.f, 0.f, 0.f, 0.f};
+    float4 cg[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cg[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (act) {
+      for (int k = wid; k < n; k += nw) {
+        const float4 Rk = sm.R[k];
+        const float tk = sm.t[k];
+        const float4 tv = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(k) * ldt + j4);
+        const float4 pu = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(k) * ln + j4);
+        const float tq[4] = {tv.x, tv.y, tv.z, tv.w};
+        const float pq[4] = {pu.x, pu.y, pu.z, pu.w};
+        float ds[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool v = j4 + q < n;  // the tile and stash hold junk past column n
+          const float tt = v ? tq[q] : 0.f, pp = v ? pq[q] : 0.f;
+          const float C = dot4(Rk, Rj[q]);
+          const float dP = tt * C * inv_sig;
+          const float dC = tt * (sj2[q] * pp) * inv_sig;
+          const float dpt = dP - tk;
+          cw[q] += pp * dpt;
+          ds[q] = sj2[q] * pp * dpt;
+          cg[q].x += dC * Rk.x;
+          cg[q].y += dC * Rk.y;
+          cg[q].z += dC * Rk.z;
+          cg[q].w += dC * Rk.w;
+        }
+        *reinterpret_cast<float4*>(DS + static_cast<size_t>(k) * ln + j4) = make_float4(ds[0], ds[1], ds[2], ds[3]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pg[wid * 128 + 4 * lane + q] = cg[q];
+        pw[wid * 128 + 4 * lane + q] = cw[q];
+      }
+    }
+    __syncthreads();
+    const float dsig = static_cast<float>(sm.red[0]);
+    for (int j = c0 + threadIdx.x; j < min(n, c0 + 128); j += blockDim.x) {
+      float dw = 0.f;
+      float4 r = sm.dR[j];
+      for (int w = 0; w < nw; ++w) {
+        const float4 p = pg[w * 128 + j - c0];
+        r.x += p.x;
+        r.y += p.y;
+        r.z += p.z;
+        r.w += p.w;
+        dw += pw[w * 128 + j - c0];
+      }
+      sm.dsx[j] += 2.f * sm.s[j] * (dw + dsig);
+      sm.dR[j] = r;
+    }
+    __syncthreads();
+  }
+  tc::fence_proxy_async();  // part sits in an operand stage that bulk copies overwrite later
 }
 
 // Row and column passes in one sweep over dP~ (n <= 128, blockDim <= 256): warp per query
@@ -1066,7 +1157,8 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         pc.mark(5);
         bwd_row_pass(n, ln, sl.T, ln, PUl, inv_sig, sm);
         __syncthreads();
-        bwd_col_pass(n, ln, n, sl.T, ln, PUl, sl.T, inv_sig, sm, sm.part);
+        if constexpr (MODE != 0) bwd_colwin_pass(n, ln, sl.T, ln, PUl, sl.T, inv_sig, sm, sm.part);
+        else bwd_col_pass(n, ln, n, sl.T, ln, PUl, sl.T, inv_sig, sm, sm.part);
       }
       __syncthreads();
       pc.mark(7);
