@@ -31,4 +31,11 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_centre_(forward|backward)" -c 2 \
   -o gpurun_out/${T}_centre python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/${T}_ncu_centre.log 2>&1
 fi
-ls gpurun_out | head -80
+# summarise on the box (reports exceed the 64 MiB copy-back limit): launch list, key
+# metrics per captured kernel, per-line stalls of the backward; then drop the reports
+python tools/summarize_ncu.py ${T} > gpurun_out/${T}_summarize.log 2>&1
+cp profiles/${T}_launches.txt profiles/${T}_ncu.txt profiles/${T}_ncu.json profiles/ncu_latest.json gpurun_out/ 2>/dev/null
+[ -f gpurun_out/${T}_centre.ncu-rep ] && python tools/ncu_lines.py gpurun_out/${T}_centre.ncu-rep 60 k_centre_backward > gpurun_out/${T}_bwd_lines.txt 2>&1
+[ -f gpurun_out/${T}_centre.ncu-rep ] && python tools/ncu_lines.py gpurun_out/${T}_centre.ncu-rep 40 k_centre_forward > gpurun_out/${T}_fwd_lines.txt 2>&1
+rm -f gpurun_out/*.ncu-rep gpurun_out/${T}_launches.csv
+du -sh gpurun_out; ls gpurun_out | head -80
