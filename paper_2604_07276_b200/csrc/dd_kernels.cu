@@ -8,6 +8,7 @@
 #include <climits>
 
 #include <algorithm>
+#include <cstdint>
 #include <type_traits>
 
 #include "common.cuh"
@@ -93,7 +94,10 @@ void launch_dd_flags(const SysArgs& s, const RankArgs& r, const int* owner, int*
   k_dd_flags<<<(s.n + 255) / 256, 256, 0, st>>>(s, r, owner, is_local, gcount); count_launch();
 }
 
-// Single-CTA exclusive scan (n up to a few 1e5; one launch, no host round trip).
+// Single-CTA exclusive scan (n up to a few 1e5; one launch, no host round trip).  Each
+// thread takes 4 consecutive elements per pass (one 16-byte load when aligned), so a pass
+// covers 4096 elements: a 28k-element scan is 7 passes of (local prefix, warp shuffle
+// scan, block scan of the warp totals).
 __global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ in, int* __restrict__ out,
                                                int n) {
   __shared__ int warp_tot[32];
@@ -101,10 +105,22 @@ __global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ in, int* 
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < n; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int v = i < n ? in[i] : 0;
-    int x = v;
+  const bool vec = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  for (int base = 0; base < n; base += 4096) {
+    const int i0 = base + 4 * threadIdx.x;
+    int v[4];
+    if (vec && i0 + 3 < n) {
+      const int4 q = *reinterpret_cast<const int4*>(in + i0);
+      v[0] = q.x;
+      v[1] = q.y;
+      v[2] = q.z;
+      v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = i0 + u < n ? in[i0 + u] : 0;
+    }
+    const int tsum = v[0] + v[1] + v[2] + v[3];
+    int x = tsum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -122,10 +138,14 @@ __global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ in, int* 
       warp_tot[lane] = t;
     }
     __syncthreads();
-    const int excl = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + x - v;
-    if (i < n) out[i] = excl;
+    int run = carry + (wid > 0 ? warp_tot[wid - 1] : 0) + x - tsum;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + u < n) out[i0 + u] = run;
+      run += v[u];
+    }
     __syncthreads();
-    if (threadIdx.x == 1023) carry = excl + v;
+    if (threadIdx.x == 1023) carry = run;
     __syncthreads();
   }
   if (threadIdx.x == 0) out[n] = carry;
@@ -282,61 +302,62 @@ void launch_cell_fill(const int* m_cell, int n, const int* start, int* fill, int
 // ----------------------------------------------------------------------------------
 constexpr int kNbrWarps = 4;
 
+// 16-byte shared-memory entry per kept candidate (small entries keep more warps resident:
+// the kernel is latency-bound).  j = candidate index in the cell-ordered arrays (member,
+// gid, position and shift are re-read from there when needed).
 struct NbrEntry {
-  double r2;
-  int64_t gid;
   uint64_t key;  // (species << 58) | (bits(r2) - kbase): same order as (species, r2)
-  int member;
+  int j;
   int species;
 };
-// centre lists also keep the image delta centre -> neighbour for their env rows
-struct NbrEntryEnv : NbrEntry {
-  double d[3];
-};
 
-__device__ __forceinline__ bool key_less(const NbrEntry& a, const NbrEntry& b) {
-  if (a.species != b.species) return a.species < b.species;
-  if (a.r2 != b.r2) return a.r2 < b.r2;
-  return a.gid < b.gid;
+// Image delta centre -> candidate j, exactly as the distance test formed it.
+__device__ __forceinline__ void cand_delta(const NbrArgs& a, int j, const double (&pc)[3], const int (&csh)[3],
+                                           double (&d)[3]) {
+  const int sj = a.cs.shift[j];
+  d[0] = image_delta(a.cs.x[j], pc[0], shift_x(sj) - csh[0], a.L[0]);
+  d[1] = image_delta(a.cs.y[j], pc[1], shift_y(sj) - csh[1], a.L[1]);
+  d[2] = image_delta(a.cs.z[j], pc[2], shift_z(sj) - csh[2], a.L[2]);
+}
+
+// Full canonical order (species, r2, gid) of deeppot.cpp:141-148 with r2 recomputed and the
+// gid loaded: for lists with an exact key tie or a key that does not pack (rare).
+__device__ __forceinline__ bool full_less(const NbrArgs& a, const NbrEntry& x, const NbrEntry& y,
+                                          const double (&pc)[3], const int (&csh)[3]) {
+  if (x.species != y.species) return x.species < y.species;
+  double dx[3], dy[3];
+  cand_delta(a, x.j, pc, csh, dx);
+  cand_delta(a, y.j, pc, csh, dy);
+  const double rx = norm2_exact(dx[0], dx[1], dx[2]), ry = norm2_exact(dy[0], dy[1], dy[2]);
+  if (rx != ry) return rx < ry;
+  return a.cs.gid[x.j] < a.cs.gid[y.j];
 }
 
 // Environment matrix of one canonical row (prepare_rows + switch_eval, dp_core.hpp:116-137,
-// 200-223), fused into the centre-list build: r and s(r) in exact FP64 from the image
-// delta the distance test already formed, env row R = (s, s/r d) as one 16-byte store,
+// 200-223), fused into the centre-list build: the image delta re-formed as the distance
+// test formed it, r and s(r) in exact FP64, env row R = (s, s/r d) as one 16-byte store,
 // the neighbour's species; returns s^2 for sigma.
-__device__ __forceinline__ double env_row(const NbrArgs& a, int li, int k, const NbrEntryEnv& e) {
-  const double r = sqrt(e.r2);
+__device__ __forceinline__ double env_row(const NbrArgs& a, int li, int k, const NbrEntry& e, const double (&pc)[3],
+                                          const int (&csh)[3]) {
+  double d[3];
+  cand_delta(a, e.j, pc, csh, d);
+  const double r = sqrt(norm2_exact(d[0], d[1], d[2]));
   double sw, ds;
   switch_fn(r, a.rcs, a.rc, sw, ds);
   const double sr = sw / r;
   const size_t o = static_cast<size_t>(li) * a.n_max + k;
-  a.R[o] = make_float4(static_cast<float>(sw), static_cast<float>(sr * e.d[0]), static_cast<float>(sr * e.d[1]),
-                       static_cast<float>(sr * e.d[2]));
+  a.R[o] = make_float4(static_cast<float>(sw), static_cast<float>(sr * d[0]), static_cast<float>(sr * d[1]),
+                       static_cast<float>(sr * d[2]));
   a.Z[o] = e.species;
   return sw * sw;
-}
-
-// Rows of one list (each lane its entries lane, lane + 32, ... at ranks rank[]), then
-// sigma = sum_k s_k^2 (FP64, lane partials in a fixed order, then a fixed warp tree).
-template <int P>
-__device__ __forceinline__ void env_rows(const NbrArgs& a, int li, int cnt, const int (&rank)[P],
-                                         const NbrEntryEnv* buf) {
-  const int lane = threadIdx.x & 31;
-  double sig = 0.0;
-#pragma unroll
-  for (int u = 0; u < P; ++u)
-    if (lane + 32 * u < cnt) sig += env_row(a, li, rank[u], buf[lane + 32 * u]);
-  sig = warp_sum(sig);
-  if (lane == 0) a.sig[li] = sig;
 }
 
 // ENV: centre lists, which also write their environment rows (env_row).
 template <bool ENV>
 __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap) {
-  using Entry = typename std::conditional<ENV, NbrEntryEnv, NbrEntry>::type;
   extern __shared__ __align__(16) unsigned char nbr_smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  Entry* buf = reinterpret_cast<Entry*>(nbr_smem_raw) + static_cast<size_t>(wid) * cap;
+  NbrEntry* buf = reinterpret_cast<NbrEntry*>(nbr_smem_raw) + static_cast<size_t>(wid) * cap;
   const int li = blockIdx.x * kNbrWarps + wid;
   if (li >= a.n_lists) return;
   const int cm = a.centre_member ? a.centre_member[li] : li + a.member_offset;
@@ -363,27 +384,17 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
         for (int base = b; base < e; base += 32) {
           const int j = base + lane;
           bool keep = false;
-          Entry ent;
+          NbrEntry ent;
           if (j < e) {
             const int mj = a.cell_members[j];
             if (mj != cm && mj < a.cand_limit) {
-              const int sj = a.cs.shift[j];
-              const int rel[3] = {shift_x(sj) - csh[0], shift_y(sj) - csh[1], shift_z(sj) - csh[2]};
-              const double dx = image_delta(a.cs.x[j], pc[0], rel[0], a.L[0]);
-              const double dy = image_delta(a.cs.y[j], pc[1], rel[1], a.L[1]);
-              const double dz = image_delta(a.cs.z[j], pc[2], rel[2], a.L[2]);
-              const double r2 = norm2_exact(dx, dy, dz);
+              double d[3];
+              cand_delta(a, j, pc, csh, d);
+              const double r2 = norm2_exact(d[0], d[1], d[2]);
               if (r2 < a.rc2) {
                 keep = true;
-                ent.r2 = r2;
-                ent.gid = a.cs.gid[j];
-                ent.member = mj;
+                ent.j = j;
                 ent.species = a.cs.species[j];
-                if constexpr (ENV) {
-                  ent.d[0] = dx;
-                  ent.d[1] = dy;
-                  ent.d[2] = dz;
-                }
                 const uint64_t rb = static_cast<uint64_t>(__double_as_longlong(r2));
                 const bool ok = rb >= a.kbase && ent.species >= 0 && ent.species < 63;
                 packable = packable && ok;
@@ -430,9 +441,8 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
     bool fast = __all_sync(0xffffffffu, packable);
     if (fast) {
       int eq = 0;
-      const uint64_t* kb = &buf[0].key;
       for (int j = 0; j < cnt; ++j) {
-        const uint64_t o = kb[j * (sizeof(Entry) / sizeof(uint64_t))];
+        const uint64_t o = buf[j].key;
 #pragma unroll
         for (int u = 0; u < kPer; ++u)
           if (u < nu) {
@@ -449,24 +459,32 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
     if (!fast) {
       for (int u = 0; u < nu; ++u) {
         if (lane + 32 * u >= cnt) continue;
-        const Entry me = buf[lane + 32 * u];
+        const NbrEntry me = buf[lane + 32 * u];
         int r = 0;
-        for (int j = 0; j < cnt; ++j) r += key_less(buf[j], me);
+        for (int j = 0; j < cnt; ++j) r += full_less(a, buf[j], me, pc, csh);
         rank[u] = r;
       }
     }
+    double sig = 0.0;
 #pragma unroll
     for (int u = 0; u < kPer; ++u)
-      if (lane + 32 * u < cnt) out[rank[u]] = buf[lane + 32 * u].member;
-    if constexpr (ENV) env_rows(a, li, cnt, rank, buf);
+      if (lane + 32 * u < cnt) {
+        const NbrEntry me = buf[lane + 32 * u];
+        out[rank[u]] = a.cell_members[me.j];
+        if constexpr (ENV) sig += env_row(a, li, rank[u], me, pc, csh);
+      }
+    if constexpr (ENV) {
+      sig = warp_sum(sig);  // lane partials in a fixed order, then a fixed warp tree
+      if (lane == 0) a.sig[li] = sig;
+    }
   } else {
     double sig = 0.0;
     for (int i = lane; i < cnt; i += 32) {
-      const Entry me = buf[i];
+      const NbrEntry me = buf[i];
       int rank = 0;
-      for (int j = 0; j < cnt; ++j) rank += key_less(buf[j], me);
-      out[rank] = me.member;
-      if constexpr (ENV) sig += env_row(a, li, rank, me);
+      for (int j = 0; j < cnt; ++j) rank += full_less(a, buf[j], me, pc, csh);
+      out[rank] = a.cell_members[me.j];
+      if constexpr (ENV) sig += env_row(a, li, rank, me, pc, csh);
     }
     if constexpr (ENV) {
       sig = warp_sum(sig);
@@ -480,7 +498,7 @@ void launch_neighbors(const NbrArgs& a, cudaStream_t st) {
   const int cap = ((a.n_max + 1 + 31) / 32) * 32;
   const int grid = (a.n_lists + kNbrWarps - 1) / kNbrWarps;
   if (a.R) {
-    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntryEnv);
+    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry);
     ensure_smem_attr(reinterpret_cast<const void*>(k_neighbors<true>), smem);
     k_neighbors<true><<<grid, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
   } else {
@@ -784,18 +802,20 @@ __global__ void __launch_bounds__(256) k_energy_virial(const double* __restrict_
   }
 }
 
+// warp q sums component q of the block partials: lanes over blocks, then a fixed tree
 __global__ void k_energy_virial_final(const double* __restrict__ part, int nb, double* __restrict__ row) {
-  const int q = threadIdx.x;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (q >= 10) return;
   double t = 0.0;
-  for (int b = 0; b < nb; ++b) t += part[10 * b + q];
-  row[q] = t;
+  for (int b = lane; b < nb; b += 32) t += part[10 * b + q];
+  t = warp_sum(t);
+  if (lane == 0) row[q] = t;
 }
 
 void launch_energy_virial(const double* e, const double* vir, const int* counts, double* part, double* row,
                           cudaStream_t st) {
   k_energy_virial<<<kEvBlocks, 256, 0, st>>>(e, vir, counts, part); count_launch();
-  k_energy_virial_final<<<1, 32, 0, st>>>(part, kEvBlocks, row); count_launch();
+  k_energy_virial_final<<<1, 320, 0, st>>>(part, kEvBlocks, row); count_launch();
 }
 
 }  // namespace nb

@@ -1433,8 +1433,13 @@ __global__ void k_fit_splitk_sum(int M, int N, int S, const float* __restrict__ 
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const size_t MN = static_cast<size_t>(M) * N;
   if (i >= MN) return;
-  float v = P[i];
-  for (int z = 1; z < S; ++z) v += P[z * MN + i];
+  float p[kFitSplit];  // all slices' loads in flight, then a fixed-order sum
+#pragma unroll
+  for (int z = 0; z < kFitSplit; ++z) p[z] = z < S ? P[z * MN + i] : 0.f;
+  float v = p[0];
+#pragma unroll
+  for (int z = 1; z < kFitSplit; ++z)
+    if (z < S) v += p[z];
   if (epi_mode == EPI_TANH_BIAS) v = tanhf(v + bias[i % N]);
   else if (epi_mode == EPI_DTANH) v = v * (1.f - Y[i] * Y[i]);
   C[i] = v;
