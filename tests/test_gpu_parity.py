@@ -297,3 +297,25 @@ def test_multi_centre_units_match_single_centre_path(monkeypatch):
     assert abs(packed["energy"] - single["energy"]) <= 1e-6 * abs(single["energy"])
     for k in ("forces", "virial", "atom_energy"):
         assert rel_err(packed[k], single[k]) <= 1e-6, k
+
+
+def test_virial_is_strain_derivative_on_gpu():
+    """The product's virial against -dE/d(eps_ab) of the product's own energy under the
+    homogeneous strain x_a -> x_a + eps_ab x_b (non-periodic cluster, all nine components;
+    FP32 FMA network so that central differences resolve it)."""
+    g = load_golden("dd_case_0")
+    m = nb.init_model(nb.test_spec(float(g["rc"])), int(g["model_seed"]))
+    ev = nb.DeviceEvaluator(m, n_ranks=1, precision=nb.PREC_FP32_SIMT)
+    pos, sp, box = g["pos"], g["species"], g["box"]
+    free = np.array([0, 0, 0], dtype=np.uint8)
+    w = ev.compute(pos, sp, box, periodic=free)["virial"]
+    step = 1e-3
+    fd = np.zeros((3, 3))
+    for a in range(3):
+        for b in range(3):
+            pp, pm = pos.copy(), pos.copy()
+            pp[:, a] += step * pos[:, b]
+            pm[:, a] -= step * pos[:, b]
+            fd[a, b] = -(ev.compute(pp, sp, box, periodic=free)["energy"] -
+                         ev.compute(pm, sp, box, periodic=free)["energy"]) / (2 * step)
+    assert np.abs(w - fd).max() <= 2e-3 * np.abs(w).max(), (w, fd)
