@@ -2,7 +2,7 @@
 # Quick GPU iteration: parity tests, a short bench (no CPU baseline) and the per-phase
 # cycle profile of the centre kernels.  Logs under gpurun_out/.
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
-timeout 600 python -m pytest tests -q -m gpu -x ${PYTEST_ARGS:-} > gpurun_out/q_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/q_pytest.log
+timeout 600 python -m pytest tests -q -m gpu -x ${PYTEST_ARGS:-} ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/q_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/q_pytest.log
 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline ${BENCH_ARGS:-} > gpurun_out/q_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/q_bench.log
 if [ -n "${PHASES:-}" ]; then
   # phase counters are compiled out of production builds: rebuild this box's copy with them
