@@ -114,12 +114,14 @@ nnmd_status nnmd_b200_compute(nnmd_b200* ctx, int64_t n, const double* coords,
 
 /* Same evaluation on DEVICE-resident inputs/outputs (pointers on ctx's device); no bulk
  * host copies.  Host synchronisation points per call (cudaStreamSynchronize):
- *   - one per DD rank handled by this process: the locals/ghosts count read-back that
- *     sizes the rank's buffers (wide_halo adds a second, for the centre count);
- *   - with world_size > 1 and masked_reduction, one after the all-reduce of the route
- *     counts, which sizes the point-to-point ghost-force transfers;
- *   - one at the end: step flags (overflow / wrap errors and route counts, all-reduced over
- *     processes so that every process throws together) and the per-kernel event times.
+ *   - one at the end: step flags (overflow / wrap errors, ghost-capacity overflow and route
+ *     counts, all-reduced over processes so that every process throws together), the
+ *     per-rank counts and the per-kernel event times;
+ *   - with world_size > 1 and masked_reduction, one more after the all-reduce of the route
+ *     counts, which sizes the point-to-point ghost-force transfers.
+ * The DD build reads nothing back: its buffers are sized by per-rank ghost capacities and
+ * the kernels take their live counts from device memory.  When a capacity overflows
+ * (flagged on the device) the call grows it and redoes the step before returning.
  * The call returns with the stream idle.  With world_size > 1 the positions of world
  * rank 0 are broadcast to all processes (collective 1) before the DD build.
  * d_out layout (float64): [energy, virial(9), forces(3n), atom_energy(n)]. */

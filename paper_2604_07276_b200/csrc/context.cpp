@@ -118,9 +118,9 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   weights_.ensure(wh_.blob.size());
   CU(cudaMemcpy(weights_.p, wh_.blob.data(), wh_.blob.size() * sizeof(float), cudaMemcpyHostToDevice));
   build_weight_images();
-  CU(cudaMallocHost(reinterpret_cast<void**>(&h_counts_), 64 * sizeof(int)));
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_flags_), (kFlagWords + 64) * sizeof(int)));
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_rcnt_), kMaxRanks * kMaxRanks * sizeof(int)));
+  CU(cudaMallocHost(reinterpret_cast<void**>(&h_rstat_), kMaxRanks * kCntWords * sizeof(int)));
   require(o.n_ranks <= 48, "nnmd_b200: at most 48 DD ranks");
   stats_.resize(static_cast<size_t>(o.n_ranks));
   debug_.resize(static_cast<size_t>(o.n_ranks));
@@ -149,9 +149,9 @@ Context::~Context() {
   if (epoch_ev_) cudaEventDestroy(epoch_ev_);
   for (auto e : md_ev_)
     if (e) cudaEventDestroy(e);
-  if (h_counts_) cudaFreeHost(h_counts_);
   if (h_flags_) cudaFreeHost(h_flags_);
   if (h_rcnt_) cudaFreeHost(h_rcnt_);
+  if (h_rstat_) cudaFreeHost(h_rstat_);
   if (h_out_) cudaFreeHost(h_out_);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -223,6 +223,22 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   owner_.ensure(static_cast<size_t>(n) + 1);
   err_.ensure(8);
   CU(cudaMemsetAsync(err_.p, 0x7f, 8 * sizeof(int), st_));
+  rstat_.ensure(static_cast<size_t>(R) * kCntWords);
+  // ghost capacities per DD rank: kept from the last step with this atom count (grown
+  // when a step overflows them), else estimated from the halo geometry -- the ghosts of
+  // a subdomain of edges e_a with halo thickness t are about (n / R) (prod (e_a + 2t) / e_a
+  // - 1), with 50 % headroom for density fluctuations
+  if (cap_n_ != n || cap_gh_.size() != static_cast<size_t>(R)) {
+    double f = 1.0;
+    for (int a = 0; a < 3; ++a) {
+      const double e = box[a] / dims[a];
+      f *= (e + 2.0 * thickness) / e;
+    }
+    double est = static_cast<double>(n) / R * (f - 1.0) * 1.5 + 1024.0;
+    if (const char* e = getenv("NNMD_GHOST_CAP")) est = atof(e);  // tests: force the overflow / redo path
+    cap_gh_.assign(static_cast<size_t>(R), static_cast<int>(std::min(est, 27.0 * static_cast<double>(n) + 64.0)));
+    cap_n_ = n;
+  }
   SysArgs sys{};
   sys.pos = d_pos;
   sys.species = d_types;
@@ -255,9 +271,54 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
     if (r % opts_.world_size == opts_.world_rank) run_rank(r, sys, dims.data(), thickness, keep_debug_);
   launch_negate(err_.p, flags_.p, kFlagWords, st_);
   route_and_reduce(n, d_out);
+  // the step's one host synchronisation (two more with several processes: the route
+  // counts, inside route_and_reduce, and none for the DD build)
   CU(cudaMemcpyAsync(h_flags_, flags_.p, (kFlagWords + opts_.n_ranks) * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CU(cudaMemcpyAsync(h_rstat_, rstat_.p, static_cast<size_t>(R) * kCntWords * sizeof(int), cudaMemcpyDeviceToHost, st_));
   CU(cudaStreamSynchronize(st_));
+  if (-h_flags_[0] != 0x7f7f7f7f) {  // bad input on any rank (k_owner), reported before anything else
+    const int atom = -h_flags_[0];
+    int sp = 0;
+    CU(cudaMemcpy(&sp, d_types + atom, sizeof sp, cudaMemcpyDeviceToHost));
+    if (sp < 0 || sp >= m.ns) throw Error("dd_evaluate: species id outside the model's species table");
+    throw Error("neighbor list: positions must be wrapped into [0, L) on periodic axes");
+  }
+  if (-h_flags_[3] != 0x7f7f7f7f) {
+    // a ghost / centre capacity overflowed on some rank: grow to the exact counts (+25 %)
+    // and redo the step (the outputs of this pass are discarded)
+    bool grown = false;
+    for (int r = 0; r < R; ++r) {
+      if (r % opts_.world_size != opts_.world_rank) continue;
+      const int* c = h_rstat_ + static_cast<size_t>(r) * kCntWords;
+      const int need = c[kCntGhExact] + (wide ? std::max(0, c[kCntCenExact] - c[kCntLoc] - c[kCntGhExact]) : 0);
+      const int cap = static_cast<int>(need * 1.25) + 1024;
+      if (cap > cap_gh_[static_cast<size_t>(r)]) {
+        cap_gh_[static_cast<size_t>(r)] = cap;
+        grown = true;
+      }
+    }
+    // with several processes another process may be the one that overflowed: every process
+    // redoes the step (the flags are all-reduced), growing all its capacities
+    if (!grown)
+      for (auto& c : cap_gh_) c = static_cast<int>(c * 1.5) + 1024;
+    require(redo_depth_ < 4, "nnmd_b200: ghost capacity did not converge");
+    ++redo_depth_;
+    struct Reset {
+      int& d;
+      ~Reset() { --d; }
+    } reset{redo_depth_};
+    compute_device(n, d_pos, d_types, d_gid, box, periodic, d_out);
+    return;
+  }
   collect_times();
+  for (int r = 0; r < R; ++r) {
+    if (r % opts_.world_size != opts_.world_rank) continue;
+    const int* c = h_rstat_ + static_cast<size_t>(r) * kCntWords;
+    RankStat& st = stats_[static_cast<size_t>(r)];
+    st.counts[0] = c[kCntLoc];
+    st.counts[1] = c[kCntGh];
+    st.counts[2] = c[kCntCen];
+  }
   if (opts_.scheme == NNMD_MASKED_REDUCTION)
     for (int r = 0; r < opts_.n_ranks; ++r) stats_[static_cast<size_t>(r)].counts[3] = h_flags_[kFlagWords + r];
   if (use_nccl_) {
@@ -412,7 +473,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   gcount_.ensure(n + 1);
   loc_off_.ensure(n + 1);
   gh_off_.ensure(n + 1);
-  counts_.ensure(8);
+  counts_.ensure(kCntWords);
   tic("dd_flags");
   launch_dd_flags(sys, ra, owner_.p, is_local_.p, gcount_.p, st_);
   toc();
@@ -420,22 +481,15 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   launch_scan(is_local_.p, loc_off_.p, n, st_);
   launch_scan(gcount_.p, gh_off_.p, n, st_);
   toc();
-  CU(cudaMemsetAsync(counts_.p, 0, 8 * sizeof(int), st_));
-  CU(cudaMemcpyAsync(counts_.p + 0, loc_off_.p + n, sizeof(int), cudaMemcpyDeviceToDevice, st_));
-  CU(cudaMemcpyAsync(counts_.p + 1, gh_off_.p + n, sizeof(int), cudaMemcpyDeviceToDevice, st_));
-  CU(cudaMemcpyAsync(h_counts_, counts_.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st_));
-  CU(cudaMemcpyAsync(h_counts_ + 4, err_.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
-  CU(cudaStreamSynchronize(st_));
-  if (h_counts_[4] != 0x7f7f7f7f) {
-    const int atom = h_counts_[4];
-    int sp = 0;
-    double p[3];
-    CU(cudaMemcpy(&sp, sys.species + atom, sizeof sp, cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(p, sys.pos + 3 * static_cast<size_t>(atom), sizeof p, cudaMemcpyDeviceToHost));
-    if (sp < 0 || sp >= m.ns) throw Error("dd_evaluate: species id outside the model's species table");
-    throw Error("neighbor list: positions must be wrapped into [0, L) on periodic axes");
-  }
-  const int nloc = h_counts_[0], ngh = h_counts_[1], nm = nloc + ngh;
+  // No host read-back here: every buffer below is sized by a capacity (locals <= n, ghosts
+  // <= cap_gh_[rank], centres <= n, or <= members for wide_halo) and every kernel takes its
+  // live counts from counts_ on the device.  An overflowing capacity is flagged (err_[3])
+  // and the step is redone with exact sizes (compute_device); bad input (err_[0]) raises
+  // at the step's end.
+  const int ngh = cap_gh_[static_cast<size_t>(rank)];  // capacities
+  const int nloc = n;
+  const int nm = nloc + ngh;
+  launch_rank_counts(loc_off_.p, gh_off_.p, n, nm, ngh, counts_.p, err_.p + 3, st_);
   m_atom_.ensure(nm + 1);
   m_shift_.ensure(nm + 1);
   m_owner_.ensure(nm + 1);
@@ -446,21 +500,14 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   cen_member_.ensure(nm + 1);
   cidx_.ensure(nm + 1);
   tic("dd_members");
-  launch_dd_members(sys, ra, owner_.p, loc_off_.p, gh_off_.p, n, m_atom_.p, m_shift_.p, m_pos_.p,
+  launch_dd_members(sys, ra, owner_.p, loc_off_.p, gh_off_.p, n, nm, m_atom_.p, m_shift_.p, m_pos_.p,
                     m_owner_.p, st_);
   launch_centre_flags(ra, counts_.p, m_pos_.p, nm, cflag_.p, st_);
-  launch_scan(cflag_.p, coff_.p, nm, st_);
-  launch_centre_compact(cflag_.p, coff_.p, nm, cen_member_.p, cidx_.p, st_);
+  launch_scan_dev(cflag_.p, coff_.p, counts_.p + kCntMem, st_);
+  const int ncen = wide ? nm : nloc;  // capacity
+  launch_centre_compact(cflag_.p, coff_.p, counts_.p, nm, wide, ncen, cen_member_.p, cidx_.p, err_.p + 3, st_);
   toc();
-  int ncen = nloc;
-  if (wide) {
-    CU(cudaMemcpyAsync(h_counts_ + 2, coff_.p + nm, sizeof(int), cudaMemcpyDeviceToHost, st_));
-    CU(cudaStreamSynchronize(st_));
-    ncen = h_counts_[2];
-  }
-  stat.counts[0] = nloc;
-  stat.counts[1] = ngh;
-  stat.counts[2] = ncen;
+  (void)stat;  // counts are read back with the step flags (compute_device)
   phases_.push_back({rank, 0, ph_dd0, timers_.size() - 1});
 
   // ---- cell grid + neighbour rows ------------------------------------------------------
@@ -493,12 +540,13 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   csd.shift = cs_i_.p;
   csd.species = cs_i_.p + nm;
   csd.gid = cs_gid_.p;
+  csd.n_species = m.ns;
   tic("cells");
   CU(cudaMemsetAsync(cell_count_.p, 0, (ncell + 1) * sizeof(int), st_));
   CU(cudaMemsetAsync(cell_fill_.p, 0, (ncell + 1) * sizeof(int), st_));
-  launch_cell_count(cg, m_pos_.p, nm, m_cell_.p, cell_count_.p, st_);
+  launch_cell_count(cg, m_pos_.p, counts_.p + kCntMem, nm, m_cell_.p, cell_count_.p, st_);
   launch_scan(cell_count_.p, cell_start_.p, static_cast<int>(ncell), st_);
-  launch_cell_fill(m_cell_.p, nm, cell_start_.p, cell_fill_.p, cell_members_.p, csd, st_);
+  launch_cell_fill(m_cell_.p, counts_.p + kCntMem, nm, cell_start_.p, cell_fill_.p, cell_members_.p, csd, st_);
   toc();
   const int nmax = m.n_max;
   nlist_.ensure(static_cast<size_t>(ncen) * nmax + 1);
@@ -529,6 +577,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   }
   na.centre_member = cen_member_.p;
   na.n_lists = ncen;
+  na.n_lists_dev = counts_.p + kCntCen;
   na.cand_limit = INT_MAX;
   na.nlist = nlist_.p;
   na.nn = nn_.p;
@@ -555,13 +604,16 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     NbrArgs rv = na;
     rv.centre_member = nullptr;
     rv.member_offset = nloc;
+    rv.member_offset_dev = counts_.p + kCntLoc;
     rv.n_lists = ngh;
+    rv.n_lists_dev = counts_.p + kCntGh;
     rv.cand_limit = nloc;
+    rv.cand_limit_dev = counts_.p + kCntLoc;
     rv.maxn = nullptr;
     rv.nlist = rlist_.p;
     rv.nn = rn_.p;
     rv.err = err_.p + 2;
-    rv.nonempty = counts_.p + 3;
+    rv.nonempty = counts_.p + kCntRoute;
     rv.R = nullptr;  // reverse lists carry no env rows
     rv.Z = nullptr;
     rv.sig = nullptr;
@@ -606,6 +658,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   dp.m_shift = m_shift_.p;
   dp.cen_member = cen_member_.p;
   dp.n_centres = ncen;
+  dp.n_centres_dev = counts_.p + kCntCen;
   dp.nlist = nlist_.p;
   dp.nn = nn_.p;
   Ad_.ensure(static_cast<size_t>(ncen) * M * 4 + 4);
@@ -653,10 +706,10 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   if (pack && ncen > 0) {
     units = pack_capacity(ncen);
     const int ng = (ncen + 3) / 4;
-    pack_cnt_.ensure(2 * static_cast<size_t>(ng) + 2);
+    pack_cnt_.ensure(2 * static_cast<size_t>(ng) + 3);
     packs_.ensure(static_cast<size_t>(units) + 1);
     tic("pack_plan");
-    launch_pack_plan(nn_.p, ncen, pack_cnt_.p, pack_cnt_.p + ng + 1, packs_.p, st_);
+    launch_pack_plan(nn_.p, counts_.p + kCntCen, ncen, pack_cnt_.p, pack_cnt_.p + ng + 1, packs_.p, st_);
     toc();
     dp.packs = packs_.p;
     dp.n_units_dev = pack_cnt_.p + ng + 1 + ng;
@@ -732,6 +785,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
     fa.fb[l] = dp.fb[l];
   }
   fa.n_centres = ncen;
+  fa.n_centres_dev = counts_.p + kCntCen;
   fa.D = D_.p;
   fa.delta[0] = fitd_.p;
   fa.delta[1] = fitd_.p + static_cast<size_t>(maxw) * ncen;
@@ -782,6 +836,8 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   fo.cidx = cidx_.p;
   fo.rlist = wide ? nullptr : rlist_.p;
   fo.rn = wide ? nullptr : rn_.p;
+  fo.counts = counts_.p;
+  fo.wide = wide;
   fo.nloc = nloc;
   fo.n_targets = wide ? nloc : nm;
   fo.g = g_.p;
@@ -798,6 +854,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   ro.wide = wide;
   ro.nloc = nloc;
   ro.ngh = ngh;
+  ro.counts = counts_.p;
   ro.m_atom = m_atom_.p;
   ro.m_shift = m_shift_.p;
   ro.m_owner = m_owner_.p;
@@ -817,10 +874,16 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   toc();
   phases_.push_back({rank, 3, ph_f0, timers_.size() - 1});
   if (!wide)
-    CU(cudaMemcpyAsync(flags_.p + kFlagWords + rank, counts_.p + 3, sizeof(int), cudaMemcpyDeviceToDevice, st_));
+    CU(cudaMemcpyAsync(flags_.p + kFlagWords + rank, counts_.p + kCntRoute, sizeof(int), cudaMemcpyDeviceToDevice, st_));
+  // the rank's counts, read back with the step flags
+  CU(cudaMemcpyAsync(rstat_.p + static_cast<size_t>(rank) * kCntWords, counts_.p, kCntWords * sizeof(int),
+                     cudaMemcpyDeviceToDevice, st_));
 
   if (keep_debug) {
+    int hc[kCntWords];
+    CU(cudaMemcpyAsync(hc, counts_.p, sizeof hc, cudaMemcpyDeviceToHost, st_));
     CU(cudaStreamSynchronize(st_));
+    const int nloc = hc[kCntLoc], ngh = hc[kCntGh], nm = nloc + ngh, ncen = hc[kCntCen];
     RankDebug& d = debug_[static_cast<size_t>(rank)];
     std::vector<int> cm(ncen), mat(nm), msh(nm), mown(nm);
     d.nn.assign(ncen, 0);

@@ -166,8 +166,13 @@ class Context {
   DevBuf<const RouteEntry*> inc_;
   long route_cap_ = 0;       // entries in the local send buffers this step
   int* h_rcnt_ = nullptr;    // pinned [R][R]
+  // ghost capacities per DD rank (no host read-back of counts inside a step)
+  std::vector<int> cap_gh_;
+  long cap_n_ = -1;
+  int redo_depth_ = 0;
+  DevBuf<int> rstat_;        // [R][kCntWords] per-rank device counts of the step
+  int* h_rstat_ = nullptr;   // pinned copy
   void route_and_reduce(long n, double* d_out);
-  int* h_counts_ = nullptr;  // pinned
   std::vector<RankStat> stats_;
   std::vector<RankDebug> debug_;
   std::vector<Timer> timers_;

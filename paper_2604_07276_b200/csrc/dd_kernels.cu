@@ -99,9 +99,10 @@ void launch_dd_flags(const SysArgs& s, const RankArgs& r, const int* owner, int*
 // covers 4096 elements: a 28k-element scan is 7 passes of (local prefix, warp shuffle
 // scan, block scan of the warp totals).
 __global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ in, int* __restrict__ out,
-                                               int n) {
+                                               int n, const int* __restrict__ n_dev) {
   __shared__ int warp_tot[32];
   __shared__ int carry;
+  if (n_dev) n = *n_dev;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -152,13 +153,17 @@ __global__ void __launch_bounds__(1024) k_scan(const int* __restrict__ in, int* 
 }
 
 void launch_scan(const int* in, int* out, int n, cudaStream_t st) {
-  k_scan<<<1, 1024, 0, st>>>(in, out, n); count_launch();
+  k_scan<<<1, 1024, 0, st>>>(in, out, n, nullptr); count_launch();
+}
+
+void launch_scan_dev(const int* in, int* out, const int* n_dev, cudaStream_t st) {
+  k_scan<<<1, 1024, 0, st>>>(in, out, 0, n_dev); count_launch();
 }
 
 // Members: locals first (ascending atom, shift 0), then ghosts in (atom, shift) order.
 __global__ void k_dd_members(SysArgs s, RankArgs r, const int* __restrict__ owner,
                              const int* __restrict__ loc_off, const int* __restrict__ gh_off,
-                             int n_atoms, int* __restrict__ m_atom, int* __restrict__ m_shift,
+                             int n_atoms, int cap, int* __restrict__ m_atom, int* __restrict__ m_shift,
                              double* __restrict__ m_pos, int* __restrict__ m_owner) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= s.n) return;
@@ -182,6 +187,7 @@ __global__ void k_dd_members(SysArgs s, RankArgs r, const int* __restrict__ owne
                              __dadd_rn(p[1], __dmul_rn(static_cast<double>(ky), s.L[1])),
                              __dadd_rn(p[2], __dmul_rn(static_cast<double>(kz), s.L[2]))};
         if (!in_slab(q, r.slab_lo, r.slab_hi)) continue;
+        if (m >= cap) continue;  // capacity overflow: reported by k_rank_counts, step redone
         m_atom[m] = i;
         m_shift[m] = pack_shift(kx, ky, kz);
         m_owner[m] = owner[i];
@@ -191,11 +197,30 @@ __global__ void k_dd_members(SysArgs s, RankArgs r, const int* __restrict__ owne
 }
 
 void launch_dd_members(const SysArgs& s, const RankArgs& r, const int* owner, const int* loc_off,
-                       const int* gh_off, int n_atoms, int* m_atom, int* m_shift, double* m_pos,
-                       int* m_owner, cudaStream_t st) {
+                       const int* gh_off, int n_atoms, int cap_members, int* m_atom, int* m_shift,
+                       double* m_pos, int* m_owner, cudaStream_t st) {
   if (s.n == 0) return;
-  k_dd_members<<<(s.n + 255) / 256, 256, 0, st>>>(s, r, owner, loc_off, gh_off, n_atoms, m_atom,
+  k_dd_members<<<(s.n + 255) / 256, 256, 0, st>>>(s, r, owner, loc_off, gh_off, n_atoms, cap_members, m_atom,
                                                   m_shift, m_pos, m_owner); count_launch();
+}
+
+__global__ void k_rank_counts(const int* __restrict__ loc_off, const int* __restrict__ gh_off, int n, int cap,
+                              int cap_gh, int* __restrict__ counts, int* __restrict__ overflow) {
+  const int nloc = loc_off[n], ngh = gh_off[n];
+  const int gh = min(min(ngh, cap_gh), max(0, cap - nloc));
+  if (gh < ngh) *overflow = 1;
+  counts[kCntLoc] = nloc;
+  counts[kCntGh] = gh;
+  counts[kCntMem] = nloc + gh;
+  counts[kCntCen] = nloc;
+  counts[kCntRoute] = 0;
+  counts[kCntGhExact] = ngh;
+  counts[kCntCenExact] = nloc;
+}
+
+void launch_rank_counts(const int* loc_off, const int* gh_off, int n_atoms, int cap_members, int cap_ghosts,
+                        int* counts, int* overflow, cudaStream_t st) {
+  k_rank_counts<<<1, 1, 0, st>>>(loc_off, gh_off, n_atoms, cap_members, cap_ghosts, counts, overflow); count_launch();
 }
 
 // Centres: every local; for wide_halo also the first-layer ghosts (inside the rc slab,
@@ -218,10 +243,18 @@ void launch_centre_flags(const RankArgs& r, const int* counts, const double* m_p
 }
 
 __global__ void k_centre_compact(const int* __restrict__ flag, const int* __restrict__ off,
-                                 int n, int* __restrict__ cen_member, int* __restrict__ cidx) {
+                                 int* __restrict__ counts, int wide, int cap_cen, int* __restrict__ cen_member,
+                                 int* __restrict__ cidx, int* __restrict__ overflow) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = counts[kCntMem];
+  if (m == 0 && wide) {
+    const int nc = off[n];
+    counts[kCntCenExact] = nc;
+    counts[kCntCen] = min(nc, cap_cen);
+    if (nc > cap_cen) *overflow = 1;
+  }
   if (m >= n) return;
-  if (flag[m]) {
+  if (flag[m] && off[m] < cap_cen) {
     cen_member[off[m]] = m;
     cidx[m] = off[m];
   } else {
@@ -229,10 +262,12 @@ __global__ void k_centre_compact(const int* __restrict__ flag, const int* __rest
   }
 }
 
-void launch_centre_compact(const int* flag, const int* off, int n_members, int* cen_member,
-                           int* cidx, cudaStream_t st) {
-  if (n_members == 0) return;
-  k_centre_compact<<<(n_members + 255) / 256, 256, 0, st>>>(flag, off, n_members, cen_member, cidx); count_launch();
+void launch_centre_compact(const int* flag, const int* off, const int* counts, int n_members_cap, int wide,
+                           int cap_centres, int* cen_member, int* cidx, int* overflow, cudaStream_t st) {
+  if (n_members_cap == 0) return;
+  k_centre_compact<<<(n_members_cap + 255) / 256, 256, 0, st>>>(flag, off, const_cast<int*>(counts), wide,
+                                                                cap_centres, cen_member, cidx, overflow);
+  count_launch();
 }
 
 // ----------------------------------------------------------------------------------
@@ -251,29 +286,30 @@ __device__ __forceinline__ int cell_of(const CellArgs& c, const double* q) {
   return (id[0] * c.dims[1] + id[1]) * c.dims[2] + id[2];
 }
 
-__global__ void k_cell_count(CellArgs c, const double* __restrict__ m_pos, int n,
+__global__ void k_cell_count(CellArgs c, const double* __restrict__ m_pos, const int* __restrict__ n_dev,
                              int* __restrict__ m_cell, int* __restrict__ count) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n) return;
+  if (m >= *n_dev) return;
   const int id = cell_of(c, m_pos + 3 * m);
   m_cell[m] = id;
   atomicAdd(&count[id], 1);
 }
 
-void launch_cell_count(const CellArgs& c, const double* m_pos, int n, int* m_cell, int* count,
-                       cudaStream_t st) {
-  if (n == 0) return;
-  k_cell_count<<<(n + 255) / 256, 256, 0, st>>>(c, m_pos, n, m_cell, count); count_launch();
+void launch_cell_count(const CellArgs& c, const double* m_pos, const int* n_dev, int n_cap, int* m_cell,
+                       int* count, cudaStream_t st) {
+  if (n_cap == 0) return;
+  k_cell_count<<<(n_cap + 255) / 256, 256, 0, st>>>(c, m_pos, n_dev, m_cell, count); count_launch();
 }
 
 // Fill the cell lists and a cell-ordered copy of what the neighbour scan reads per
 // candidate (atom position, packed shift, species, gid), so that scan's loads are
 // contiguous across a warp instead of chasing member -> atom indirections.  The order
 // inside a cell is arbitrary: rows are sorted by the canonical key afterwards.
-__global__ void k_cell_fill(const int* __restrict__ m_cell, int n, const int* __restrict__ start,
-                            int* __restrict__ fill, int* __restrict__ members, CellSorted cs) {
+__global__ void k_cell_fill(const int* __restrict__ m_cell, const int* __restrict__ n_dev,
+                            const int* __restrict__ start, int* __restrict__ fill, int* __restrict__ members,
+                            CellSorted cs) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n) return;
+  if (m >= *n_dev) return;
   const int id = m_cell[m];
   const int slot = atomicAdd(&fill[id], 1);
   const int j = start[id] + slot;
@@ -283,14 +319,14 @@ __global__ void k_cell_fill(const int* __restrict__ m_cell, int n, const int* __
   cs.y[j] = cs.pos[3 * aj + 1];
   cs.z[j] = cs.pos[3 * aj + 2];
   cs.shift[j] = cs.m_shift[m];
-  cs.species[j] = cs.atom_species[aj];
+  cs.species[j] = min(max(cs.atom_species[aj], 0), cs.n_species - 1);
   cs.gid[j] = cs.atom_gid[aj];
 }
 
-void launch_cell_fill(const int* m_cell, int n, const int* start, int* fill, int* members, const CellSorted& cs,
-                      cudaStream_t st) {
-  if (n == 0) return;
-  k_cell_fill<<<(n + 255) / 256, 256, 0, st>>>(m_cell, n, start, fill, members, cs); count_launch();
+void launch_cell_fill(const int* m_cell, const int* n_dev, int n_cap, const int* start, int* fill, int* members,
+                      const CellSorted& cs, cudaStream_t st) {
+  if (n_cap == 0) return;
+  k_cell_fill<<<(n_cap + 255) / 256, 256, 0, st>>>(m_cell, n_dev, start, fill, members, cs); count_launch();
 }
 
 // ----------------------------------------------------------------------------------
@@ -359,8 +395,9 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   NbrEntry* buf = reinterpret_cast<NbrEntry*>(nbr_smem_raw) + static_cast<size_t>(wid) * cap;
   const int li = blockIdx.x * kNbrWarps + wid;
-  if (li >= a.n_lists) return;
-  const int cm = a.centre_member ? a.centre_member[li] : li + a.member_offset;
+  if (li >= (a.n_lists_dev ? *a.n_lists_dev : a.n_lists)) return;
+  const int cm = a.centre_member ? a.centre_member[li]
+                                 : li + (a.member_offset_dev ? *a.member_offset_dev : a.member_offset);
   const int ca = a.m_atom[cm];
   const int cs = a.m_shift[cm];
   const double pc[3] = {a.pos[3 * ca], a.pos[3 * ca + 1], a.pos[3 * ca + 2]};
@@ -368,6 +405,7 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
   const int cell = a.m_cell[cm];
   const int cz = cell % a.cdims[2], cy = (cell / a.cdims[2]) % a.cdims[1],
             cx = cell / (a.cdims[1] * a.cdims[2]);
+  const int cand_limit = a.cand_limit_dev ? *a.cand_limit_dev : a.cand_limit;
   int cnt = 0;
   bool packable = true;  // every kept key fits the 64-bit packing (per lane)
   for (int ox = -1; ox <= 1; ++ox) {
@@ -387,7 +425,7 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
           NbrEntry ent;
           if (j < e) {
             const int mj = a.cell_members[j];
-            if (mj != cm && mj < a.cand_limit) {
+            if (mj != cm && mj < cand_limit) {
               double d[3];
               cand_delta(a, j, pc, csh, d);
               const double r2 = norm2_exact(d[0], d[1], d[2]);
@@ -519,7 +557,8 @@ void launch_neighbors(const NbrArgs& a, cudaStream_t st) {
 __global__ void __launch_bounds__(128) k_force_gather(ForceArgs a) {
   const int lane = threadIdx.x & 31;
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (t >= a.n_targets) return;
+  const int nloc = a.counts[kCntLoc];
+  if (t >= (a.wide ? nloc : a.counts[kCntMem])) return;
   double own[3] = {0, 0, 0};
   const int oc = a.cidx[t];
   if (oc >= 0) {
@@ -530,12 +569,12 @@ __global__ void __launch_bounds__(128) k_force_gather(ForceArgs a) {
   }
   const int* list;
   int cnt;
-  if (t < a.nloc) {
+  if (t < nloc) {
     list = a.nlist + static_cast<size_t>(oc) * a.n_max;
     cnt = a.nn[oc];
   } else {
-    list = a.rlist + static_cast<size_t>(t - a.nloc) * a.n_max;
-    cnt = a.rn[t - a.nloc];
+    list = a.rlist + static_cast<size_t>(t - nloc) * a.n_max;
+    cnt = a.rn[t - nloc];
   }
   // lane per incoming centre c: find t's row k in c's list (16-byte loads), take g[c][k]
   double in[3] = {0, 0, 0};
@@ -584,21 +623,22 @@ void launch_force_gather(const ForceArgs& a, cudaStream_t st) {
 // ----------------------------------------------------------------------------------
 __global__ void k_route_count(RouteArgs a) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= a.nloc + a.ngh) return;
-  if (m < a.nloc) {
+  const int nloc = a.counts[kCntLoc], ngh = a.counts[kCntGh];
+  if (m >= nloc + ngh) return;
+  if (m < nloc) {
     const int t = a.m_atom[m];
 #pragma unroll
     for (int q = 0; q < 3; ++q) a.fown[3 * static_cast<size_t>(t) + q] = a.fmem[3 * static_cast<size_t>(m) + q];
     a.eown[t] = a.e_centre[m];
-  } else if (!a.wide && a.rn[m - a.nloc] > 0) {
+  } else if (!a.wide && a.rn[m - nloc] > 0) {
     atomicAdd(&a.cnt[a.rank * a.n_ranks + a.m_owner[m]], 1);
   }
 }
 
 __global__ void k_route_fill(RouteArgs a) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= a.ngh || a.rn[g] == 0) return;
-  const int m = a.nloc + g;
+  if (g >= a.counts[kCntGh] || a.rn[g] == 0) return;
+  const int m = a.counts[kCntLoc] + g;
   const int o = a.m_owner[m];
   const int* row = a.cnt + a.rank * a.n_ranks;
   int off = 0;
@@ -743,21 +783,25 @@ void launch_finalize(const double* red, int n_ranks, long n_atoms, double* out, 
 // Multi-centre tiles (rc = 4: n <= 64, ~27 rows per centre): groups of four consecutive
 // centres become one 128-row unit when their rows fit, else two pairs (always fit).
 // ----------------------------------------------------------------------------------
-__device__ __forceinline__ int pack_group_units(const int* nn, int n_centres, int g) {
+__device__ __forceinline__ int pack_group_units(const int* nn, int n_centres, int g) {  // g < groups
   const int c0 = 4 * g, c1 = min(n_centres, c0 + 4);
   int rows = 0;
   for (int c = c0; c < c1; ++c) rows += nn[c];
   return (rows <= 128 || c1 - c0 <= 2) ? 1 : 2;
 }
 
-__global__ void k_pack_count(const int* __restrict__ nn, int n_centres, int* __restrict__ cnt) {
+__global__ void k_pack_count(const int* __restrict__ nn, const int* __restrict__ n_dev, int cap_groups,
+                             int* __restrict__ cnt, int* __restrict__ n_groups) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < (n_centres + 3) / 4) cnt[g] = pack_group_units(nn, n_centres, g);
+  const int n_centres = *n_dev, ng = (n_centres + 3) / 4;
+  if (g == 0) *n_groups = ng;
+  if (g < cap_groups) cnt[g] = g < ng ? pack_group_units(nn, n_centres, g) : 0;
 }
 
-__global__ void k_pack_fill(const int* __restrict__ nn, int n_centres, const int* __restrict__ off,
-                            int2* __restrict__ packs) {
+__global__ void k_pack_fill(const int* __restrict__ nn, const int* __restrict__ n_dev,
+                            const int* __restrict__ off, int2* __restrict__ packs) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_centres = *n_dev;
   if (g >= (n_centres + 3) / 4) return;
   const int c0 = 4 * g, m = min(4, n_centres - c0);
   if (pack_group_units(nn, n_centres, g) == 1) {
@@ -768,15 +812,18 @@ __global__ void k_pack_fill(const int* __restrict__ nn, int n_centres, const int
   }
 }
 
-void launch_pack_plan(const int* nn, int n_centres, int* cnt, int* off, int2* packs, cudaStream_t st) {
-  const int ng = (n_centres + 3) / 4;
-  if (ng == 0) {
+// cnt: scratch of cap_groups + 1 ints, off: of cap_groups + 2 ints (scan | unit count at
+// off[cap_groups]); groups past the live count contribute zero units
+void launch_pack_plan(const int* nn, const int* n_dev, int n_centres_cap, int* cnt, int* off, int2* packs,
+                      cudaStream_t st) {
+  const int cg = (n_centres_cap + 3) / 4;
+  if (cg == 0) {
     cudaMemsetAsync(off, 0, sizeof(int), st);
     return;
   }
-  k_pack_count<<<(ng + 255) / 256, 256, 0, st>>>(nn, n_centres, cnt); count_launch();
-  launch_scan(cnt, off, ng, st);  // off[ng] = unit count
-  k_pack_fill<<<(ng + 255) / 256, 256, 0, st>>>(nn, n_centres, off, packs); count_launch();
+  k_pack_count<<<(cg + 255) / 256, 256, 0, st>>>(nn, n_dev, cg, cnt, cnt + cg); count_launch();
+  launch_scan(cnt, off, cg, st);  // off[cg] = unit count
+  k_pack_fill<<<(cg + 255) / 256, 256, 0, st>>>(nn, n_dev, off, packs); count_launch();
 }
 
 // Two-stage deterministic reduction: block b sums the centres of its contiguous chunk

@@ -260,7 +260,7 @@ struct CentreQueue {
 // Stage centre c's env rows (written by the centre-list build, k_neighbors) into shared
 // memory; returns sigma.
 __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int& zi) {
-  zi = a.species[a.m_atom[a.cen_member[c]]];
+  zi = min(max(a.species[a.m_atom[a.cen_member[c]]], 0), a.ns - 1);  // bad input raises at the step's end
   const float4* Rg = a.R + static_cast<size_t>(c) * a.n_max;
   const int* Zg = a.Z + static_cast<size_t>(c) * a.n_max;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
@@ -287,7 +287,7 @@ __device__ int unit_rows_pack(const DpArgs& a, int u, const Smem& sm) {
       sm.pk_off[i] = off;
       const double sg = v ? a.sig[c] : 0.0;
       sm.pk_isig[i] = sg > 0.0 ? static_cast<float>(1.0 / sg) : 0.f;
-      sm.pk_zi[i] = v ? a.species[a.m_atom[a.cen_member[c]]] : 0;
+      sm.pk_zi[i] = v ? min(max(a.species[a.m_atom[a.cen_member[c]]], 0), a.ns - 1) : 0;
       off += v ? a.nn[c] : 0;
     }
     sm.pk_off[4] = off;
@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_forward(const __grid_constant
 #endif
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int ur = a.unit_rows, ur4 = (ur + 3) & ~3;
-  const int n_units = PACK ? *a.n_units_dev : a.n_centres;
+  const int n_units = PACK ? *a.n_units_dev : (a.n_centres_dev ? *a.n_centres_dev : a.n_centres);
   CentreQueue queue(a.work);
   // unit u: one centre (u = c), or a multi-centre pack (DpArgs::packs)
   for (int u = blockIdx.x; u < n_units; u = queue.next()) {
@@ -997,7 +997,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   const int M = a.M, M2 = 2 * M, mr = a.mr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int ur = a.unit_rows, ur4 = (ur + 3) & ~3;
-  const int n_units = PACK ? *a.n_units_dev : a.n_centres;
+  const int n_units = PACK ? *a.n_units_dev : (a.n_centres_dev ? *a.n_centres_dev : a.n_centres);
   CentreQueue queue(a.work);
   // unit u: one centre (u = c), or a multi-centre pack (DpArgs::packs)
   for (int u = blockIdx.x; u < n_units; u = queue.next()) {
@@ -1400,17 +1400,20 @@ __host__ __device__ inline int fit_split(int K) {
   return (K >= 1024 && (K / 128) % kFitSplit == 0) ? kFitSplit : 1;
 }
 
+// M: row capacity (grid, split-K slice stride); rows >= *M_live are not computed.
 template <bool TB, int MODE>
-__global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const float* __restrict__ A,
-                                                     const float* __restrict__ B, int ldb,
-                                                     float* __restrict__ C, const float* __restrict__ bias,
+__global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, const int* __restrict__ M_live, int N, int K,
+                                                     const float* __restrict__ A, const float* __restrict__ B,
+                                                     int ldb, float* __restrict__ C, const float* __restrict__ bias,
                                                      const float* __restrict__ Y, int epi_mode) {
   extern __shared__ __align__(1024) unsigned char fit_smem_raw[];
   unsigned char* head = fit_smem_raw + ((1024 - (tc::smem_u32(fit_smem_raw) & 1023)) & 1023);
   constexpr int TM = MODE == 0 ? kTM : tc::kMT;
   constexpr int TN = MODE == 0 ? kTN : tc::kNT;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
-  const int Ms = min(TM, M - m0), Ns = min(TN, N - n0);
+  const int Mv = M_live ? min(M, *M_live) : M;
+  if (m0 >= Mv) return;  // past the rank's live centres (the grid covers the capacity)
+  const int Ms = min(TM, Mv - m0), Ns = min(TN, N - n0);
   // split-K slice (gridDim.z > 1): raw partial tile into C's slice z, epilogue later
   const int Kc = K / static_cast<int>(gridDim.z), kz = static_cast<int>(blockIdx.z) * Kc;
   const float* Ab = A + static_cast<size_t>(m0) * K + kz;
@@ -1428,11 +1431,13 @@ __global__ void __launch_bounds__(256, 1) k_fit_gemm(int M, int N, int K, const 
   mm.finish();
 }
 
-__global__ void k_fit_splitk_sum(int M, int N, int S, const float* __restrict__ P, float* __restrict__ C,
-                                 const float* __restrict__ bias, const float* __restrict__ Y, int epi_mode) {
+__global__ void k_fit_splitk_sum(int M, const int* __restrict__ M_live, int N, int S, const float* __restrict__ P,
+                                 float* __restrict__ C, const float* __restrict__ bias, const float* __restrict__ Y,
+                                 int epi_mode) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   const size_t MN = static_cast<size_t>(M) * N;
-  if (i >= MN) return;
+  const int Mv = M_live ? min(M, *M_live) : M;
+  if (i >= static_cast<size_t>(Mv) * N) return;
   float p[kFitSplit];  // all slices' loads in flight, then a fixed-order sum
 #pragma unroll
   for (int z = 0; z < kFitSplit; ++z) p[z] = z < S ? P[z * MN + i] : 0.f;
@@ -1446,28 +1451,28 @@ __global__ void k_fit_splitk_sum(int M, int N, int S, const float* __restrict__ 
 }
 
 template <bool TB, int MODE>
-static void fit_gemm(int M, int N, int K, const float* A, const float* B, int ldb, float* C, const float* bias,
-                     const float* Y, int epi, cudaStream_t st, float* ws = nullptr, int n_sm = 0) {
+static void fit_gemm(int M, const int* M_live, int N, int K, const float* A, const float* B, int ldb, float* C,
+                     const float* bias, const float* Y, int epi, cudaStream_t st, float* ws = nullptr, int n_sm = 0) {
   constexpr int TM = MODE == 0 ? kTM : tc::kMT;
   constexpr int TN = MODE == 0 ? kTN : tc::kNT;
   const size_t smem = head_bytes(MODE, 2) + 1024;
   ensure_smem_attr(reinterpret_cast<const void*>(k_fit_gemm<TB, MODE>), smem);
   const int S = (MODE != 0 && ws && N <= TN) ? fit_split(K) : 1;
   dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, S);
-  k_fit_gemm<TB, MODE><<<grid, 256, smem, st>>>(M, N, K, A, B, ldb, S > 1 ? ws : C, bias, Y, epi);
+  k_fit_gemm<TB, MODE><<<grid, 256, smem, st>>>(M, M_live, N, K, A, B, ldb, S > 1 ? ws : C, bias, Y, epi);
   count_launch();
   if (S > 1) {
     const size_t MN = static_cast<size_t>(M) * N;
-    k_fit_splitk_sum<<<static_cast<int>((MN + 255) / 256), 256, 0, st>>>(M, N, S, ws, C, bias, Y, epi);
+    k_fit_splitk_sum<<<static_cast<int>((MN + 255) / 256), 256, 0, st>>>(M, M_live, N, S, ws, C, bias, Y, epi);
     count_launch();
   }
 }
 
 template <int MODE>
-static void fit_gemm_tb(bool tb, int M, int N, int K, const float* A, const float* B, int ldb, float* C,
-                        const float* bias, const float* Y, int epi, cudaStream_t st, float* ws, int n_sm) {
-  if (tb) fit_gemm<true, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st, ws, n_sm);
-  else fit_gemm<false, MODE>(M, N, K, A, B, ldb, C, bias, Y, epi, st, ws, n_sm);
+static void fit_gemm_tb(bool tb, int M, const int* M_live, int N, int K, const float* A, const float* B, int ldb,
+                        float* C, const float* bias, const float* Y, int epi, cudaStream_t st, float* ws, int n_sm) {
+  if (tb) fit_gemm<true, MODE>(M, M_live, N, K, A, B, ldb, C, bias, Y, epi, st, ws, n_sm);
+  else fit_gemm<false, MODE>(M, M_live, N, K, A, B, ldb, C, bias, Y, epi, st, ws, n_sm);
 }
 
 size_t fit_workspace_floats(int n_centres, int width, int) {
@@ -1475,11 +1480,12 @@ size_t fit_workspace_floats(int n_centres, int width, int) {
 }
 
 // e[c] = b + w . Y[c]   (linear output layer); delta[c][o] = w[o] (1 - Y[c][o]^2)
-__global__ void k_fit_out(int nc, int H, const float* __restrict__ Y, const float* __restrict__ w,
-                          const float* __restrict__ b, double* __restrict__ e, float* __restrict__ delta) {
+__global__ void k_fit_out(int nc, const int* __restrict__ nc_live, int H, const float* __restrict__ Y,
+                          const float* __restrict__ w, const float* __restrict__ b, double* __restrict__ e,
+                          float* __restrict__ delta) {
   const int lane = threadIdx.x & 31;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (c >= nc) return;
+  if (c >= (nc_live ? min(nc, *nc_live) : nc)) return;
   const float* y = Y + static_cast<size_t>(c) * H;
   float acc = 0.f;
   for (int o = lane; o < H; o += 32) {
@@ -1491,9 +1497,10 @@ __global__ void k_fit_out(int nc, int H, const float* __restrict__ Y, const floa
   if (lane == 0) e[c] = static_cast<double>(acc) + static_cast<double>(b[0]);
 }
 
-__global__ void k_fill_rows(int nc, int H, const float* __restrict__ w, float* __restrict__ out) {
+__global__ void k_fill_rows(int nc, const int* __restrict__ nc_live, int H, const float* __restrict__ w,
+                            float* __restrict__ out) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<size_t>(nc) * H) return;
+  if (i >= static_cast<size_t>(nc_live ? min(nc, *nc_live) : nc) * H) return;
   out[i] = w[i % H];
 }
 
@@ -1503,9 +1510,10 @@ void launch_fit(const FitArgs& a, cudaStream_t st) {
   const int L = a.n_fit;
   auto gemm = [&](bool tb, int N, int K, const float* A, const float* B, int ldb, float* C,
                   const float* bias, const float* Y, int mode) {
-    if (a.mode == 0) fit_gemm_tb<0>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st, nullptr, 0);
-    else if (a.mode == 1) fit_gemm_tb<1>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st, a.ws, a.n_sm);
-    else fit_gemm_tb<2>(tb, nc, N, K, A, B, ldb, C, bias, Y, mode, st, a.ws, a.n_sm);
+    const int* ml = a.n_centres_dev;
+    if (a.mode == 0) fit_gemm_tb<0>(tb, nc, ml, N, K, A, B, ldb, C, bias, Y, mode, st, nullptr, 0);
+    else if (a.mode == 1) fit_gemm_tb<1>(tb, nc, ml, N, K, A, B, ldb, C, bias, Y, mode, st, a.ws, a.n_sm);
+    else fit_gemm_tb<2>(tb, nc, ml, N, K, A, B, ldb, C, bias, Y, mode, st, a.ws, a.n_sm);
   };
   // forward hidden layers: Y_l = tanh(X W_l^T + b_l)
   const float* x = a.D;
@@ -1516,13 +1524,13 @@ void launch_fit(const FitArgs& a, cudaStream_t st) {
   const int H = a.fdims[L - 1];
   if (L == 1) {
     // e = b + w . D ; dD = w
-    k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, H, a.D, a.fw[0], a.fb[0], a.e, nullptr); count_launch();
-    k_fill_rows<<<static_cast<int>((static_cast<size_t>(nc) * H + 255) / 256), 256, 0, st>>>(nc, H, a.fw[0], a.dD); count_launch();
+    k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, a.n_centres_dev, H, a.D, a.fw[0], a.fb[0], a.e, nullptr); count_launch();
+    k_fill_rows<<<static_cast<int>((static_cast<size_t>(nc) * H + 255) / 256), 256, 0, st>>>(nc, a.n_centres_dev, H, a.fw[0], a.dD); count_launch();
     return;
   }
   float* dcur = a.delta[0];
   float* dnxt = a.delta[1];
-  k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, H, a.Y[L - 2], a.fw[L - 1], a.fb[L - 1], a.e, dcur); count_launch();
+  k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, a.n_centres_dev, H, a.Y[L - 2], a.fw[L - 1], a.fb[L - 1], a.e, dcur); count_launch();
   // delta_{l-1} = (delta_l W_l) o (1 - Y_{l-1}^2);  dD = delta_0 W_0
   for (int l = L - 2; l >= 1; --l) {
     gemm(false, a.fdims[l], a.fdims[l + 1], dcur, a.fw[l], a.fdims[l], dnxt, nullptr, a.Y[l - 1], EPI_DTANH);

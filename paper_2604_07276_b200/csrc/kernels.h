@@ -37,24 +37,41 @@ void launch_dd_flags(const SysArgs& s, const RankArgs& r, const int* owner, int*
                      int* gcount, cudaStream_t st);
 // exclusive scan of n ints; out[n] receives the total (out has n+1 entries)
 void launch_scan(const int* in, int* out, int n, cudaStream_t st);
+// same, n read from device memory (*n_dev) when the kernel runs
+void launch_scan_dev(const int* in, int* out, const int* n_dev, cudaStream_t st);
 // dst[i] = -src[i], i < n <= 32 (error words -> max-reducible step flags)
 void launch_negate(const int* src, int* dst, int n, cudaStream_t st);
+// Members are written only below cap_members (the buffers' capacity); launch_rank_counts
+// reports an overflow.
 void launch_dd_members(const SysArgs& s, const RankArgs& r, const int* owner, const int* loc_off,
-                       const int* gh_off, int n_atoms, int* m_atom, int* m_shift, double* m_pos,
-                       int* m_owner, cudaStream_t st);
+                       const int* gh_off, int n_atoms, int cap_members, int* m_atom, int* m_shift,
+                       double* m_pos, int* m_owner, cudaStream_t st);
+
+// Device-resident counts of one DD rank (no host read-back inside a step):
+enum { kCntLoc = 0, kCntGh = 1, kCntCen = 2, kCntRoute = 3, kCntMem = 4, kCntGhExact = 5, kCntCenExact = 6,
+       kCntWords = 8 };
+// counts[kCntLoc] = locals, [kCntGh] = ghosts (clamped to the capacity), [kCntMem] = members,
+// [kCntCen] = locals (masked scheme; wide: set by launch_centre_compact), exact ghost count
+// in [kCntGhExact]; *overflow = 1 when the ghosts exceed cap_ghosts (or the members
+// cap_members).
+void launch_rank_counts(const int* loc_off, const int* gh_off, int n_atoms, int cap_members, int cap_ghosts,
+                        int* counts, int* overflow, cudaStream_t st);
 // centre flags over members (locals always; first-layer ghosts when wide)
 void launch_centre_flags(const RankArgs& r, const int* counts /*[nloc, ngh]*/, const double* m_pos,
                          int n_members_cap, int* flag, cudaStream_t st);
-void launch_centre_compact(const int* flag, const int* off, int n_members, int* cen_member,
-                           int* cidx, cudaStream_t st);
+// over counts[kCntMem] members (grid: n_members_cap); wide_halo also sets counts[kCntCen]
+// (clamped to cap_centres, *overflow = 1 beyond it)
+void launch_centre_compact(const int* flag, const int* off, const int* counts, int n_members_cap, int wide,
+                           int cap_centres, int* cen_member, int* cidx, int* overflow, cudaStream_t st);
 
 // ---------------------------------------------------------------- cells / neighbours -
 struct CellArgs {
   double origin[3], width[3];
   int dims[3];
 };
-void launch_cell_count(const CellArgs& c, const double* m_pos, int n_members, int* m_cell,
-                       int* cell_count, cudaStream_t st);
+// over *n_members_dev members (grid: n_members_cap)
+void launch_cell_count(const CellArgs& c, const double* m_pos, const int* n_members_dev, int n_members_cap,
+                       int* m_cell, int* cell_count, cudaStream_t st);
 // cell-ordered copies of the per-candidate inputs of the neighbour scan (k_cell_fill)
 struct CellSorted {
   const double* pos;          // atom positions [n][3]
@@ -66,9 +83,11 @@ struct CellSorted {
   int* shift;
   int* species;
   int64_t* gid;
+  int n_species;              // species copies clamped into the table (bad input is reported by
+                              // k_owner and raised at the step's end; the kernels stay in bounds)
 };
-void launch_cell_fill(const int* m_cell, int n_members, const int* cell_start, int* cell_fill,
-                      int* cell_members, const CellSorted& cs, cudaStream_t st);
+void launch_cell_fill(const int* m_cell, const int* n_members_dev, int n_members_cap, const int* cell_start,
+                      int* cell_fill, int* cell_members, const CellSorted& cs, cudaStream_t st);
 
 struct NbrArgs {
   const double* pos;
@@ -84,8 +103,11 @@ struct NbrArgs {
   int cdims[3];
   const int* centre_member;  // member index of each list owner (NULL: li + member_offset)
   int member_offset;
-  int n_lists;
+  int n_lists;               // capacity (grid); the live count is *n_lists_dev
+  const int* n_lists_dev;
+  const int* member_offset_dev;  // reverse lists: *member_offset_dev (locals) instead of member_offset
   int cand_limit;            // only candidate members with index < cand_limit
+  const int* cand_limit_dev;  // (reverse lists) *cand_limit_dev instead
   int n_max;
   double rc2;
   int* nlist;                // [n_lists][n_max] member indices, canonical order
@@ -104,14 +126,16 @@ void launch_neighbors(const NbrArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- forces --------------
 struct ForceArgs {
+  const int* counts;     // device counts (kCnt*): live nloc and member count
+  int wide;
   const int* nlist;
   const int* nn;
   int n_max;
   const int* cidx;       // member -> centre index, -1 if not a centre
   const int* rlist;      // ghost reverse lists (masked), [n_ghost][n_max]
   const int* rn;
-  int nloc;
-  int n_targets;         // masked: all members; wide: locals
+  int nloc;              // (unused: device counts)
+  int n_targets;         // capacity (grid); live: masked all members, wide locals
   const double* g;       // [centre][n_max][3] row gradients de/dd_k
   double* fmem;          // [member][3] force partial
 };
@@ -138,7 +162,8 @@ static_assert(sizeof(RouteEntry) == 32, "RouteEntry is 32 bytes");
 
 struct RouteArgs {
   int rank, n_ranks, wide;
-  int nloc, ngh;
+  int nloc, ngh;            // capacities (grids); live counts from `counts`
+  const int* counts;        // device counts (kCnt*)
   const int* m_atom;
   const int* m_shift;
   const int* m_owner;
@@ -202,7 +227,8 @@ struct DpArgs {
   const int* m_atom;
   const int* m_shift;
   const int* cen_member;
-  int n_centres;
+  int n_centres;              // capacity (grids, stash strides); live count *n_centres_dev
+  const int* n_centres_dev;
   const int* nlist;
   const int* nn;
   // stash (per centre) and scratch (per CTA slot)
@@ -251,7 +277,8 @@ struct DpArgs {
 // Packs of consecutive centres (groups of 4: one pack if their rows fit 128, else two
 // pairs); units written to packs, their count to *n_units.  cnt/off: scratch of
 // ceil(n_centres/4) + 1 ints.
-void launch_pack_plan(const int* nn, int n_centres, int* cnt, int* off, int2* packs, cudaStream_t st);
+void launch_pack_plan(const int* nn, const int* n_centres_dev, int n_centres_cap, int* cnt, int* off, int2* packs,
+                      cudaStream_t st);
 inline int pack_capacity(int n_centres) { return 2 * ((n_centres + 3) / 4); }
 // Weight images: bytes for a K x N operand, and the builder (B(k,n) = TB ? W[n*ldb+k] :
 // W[k*ldb+n]).
@@ -271,7 +298,8 @@ struct FitArgs {
   int fdims[kMaxLayers + 1];
   const float* fw[kMaxLayers];
   const float* fb[kMaxLayers];
-  int n_centres;
+  int n_centres;              // capacity (grids); live count *n_centres_dev
+  const int* n_centres_dev;
   const float* D;
   float* Y[kMaxLayers];      // hidden activations [n_centres][fdims[l+1]]
   float* delta[2];           // ping-pong [n_centres][max width]

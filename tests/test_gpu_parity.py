@@ -319,3 +319,24 @@ def test_virial_is_strain_derivative_on_gpu():
             fd[a, b] = -(ev.compute(pp, sp, box, periodic=free)["energy"] -
                          ev.compute(pm, sp, box, periodic=free)["energy"]) / (2 * step)
     assert np.abs(w - fd).max() <= 2e-3 * np.abs(w).max(), (w, fd)
+
+
+@pytest.mark.parametrize("scheme", [nb.MASKED_REDUCTION, nb.WIDE_HALO])
+def test_ghost_capacity_overflow_redo(monkeypatch, scheme):
+    """The DD build has no host read-back: buffers are sized by ghost capacities and an
+    overflow is flagged on the device, then the step is redone with grown capacities.
+    A capacity of 16 ghosts forces that path; the result must equal, bit for bit, a run
+    whose first estimate fits, and the golden dd_evaluate result."""
+    g = load_golden("dd_case_0")
+    m = nb.init_model(nb.test_spec(float(g["rc"])), int(g["model_seed"]))
+    ref = nb.DeviceEvaluator(m, n_ranks=4, scheme=scheme).compute(g["pos"], g["species"], g["box"])
+    monkeypatch.setenv("NNMD_GHOST_CAP", "16")
+    ev = nb.DeviceEvaluator(m, n_ranks=4, scheme=scheme)
+    r = ev.compute(g["pos"], g["species"], g["box"])
+    for k in ("forces", "virial", "atom_energy"):
+        assert np.array_equal(r[k], ref[k]), k
+    assert r["energy"] == ref["energy"]
+    st = [ev.rank_stats(q) for q in range(4)]
+    assert all(s["ghosts"] > 16 for s in st)
+    r2 = ev.compute(g["pos"], g["species"], g["box"])  # grown capacities are kept
+    assert np.array_equal(r2["forces"], ref["forces"])
