@@ -121,6 +121,7 @@ Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) 
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_flags_), (kFlagWords + 64) * sizeof(int)));
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_rcnt_), kMaxRanks * kMaxRanks * sizeof(int)));
   CU(cudaMallocHost(reinterpret_cast<void**>(&h_rstat_), kMaxRanks * kCntWords * sizeof(int)));
+  CU(cudaMallocHost(reinterpret_cast<void**>(&h_md_err_), sizeof(int)));
   require(o.n_ranks <= 48, "nnmd_b200: at most 48 DD ranks");
   stats_.resize(static_cast<size_t>(o.n_ranks));
   debug_.resize(static_cast<size_t>(o.n_ranks));
@@ -152,6 +153,7 @@ Context::~Context() {
   if (h_flags_) cudaFreeHost(h_flags_);
   if (h_rcnt_) cudaFreeHost(h_rcnt_);
   if (h_rstat_) cudaFreeHost(h_rstat_);
+  if (h_md_err_) cudaFreeHost(h_md_err_);
   if (h_out_) cudaFreeHost(h_out_);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -275,6 +277,11 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
   // counts, inside route_and_reduce, and none for the DD build)
   CU(cudaMemcpyAsync(h_flags_, flags_.p, (kFlagWords + opts_.n_ranks) * sizeof(int), cudaMemcpyDeviceToHost, st_));
   CU(cudaMemcpyAsync(h_rstat_, rstat_.p, static_cast<size_t>(R) * kCntWords * sizeof(int), cudaMemcpyDeviceToHost, st_));
+  if (md_check_) {
+    // run_md: the finite-force check rides on the same read-back (engine.cpp:166-176)
+    launch_force_check(*md_check_, st_);
+    CU(cudaMemcpyAsync(h_md_err_, md_check_->err, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  }
   CU(cudaStreamSynchronize(st_));
   if (-h_flags_[0] != 0x7f7f7f7f) {  // bad input on any rank (k_owner), reported before anything else
     const int atom = -h_flags_[0];
@@ -1115,21 +1122,22 @@ void Context::run_md(long n, double* d_pos, double* d_vel, const double* d_mass,
   }
   ma.ke_atom = md_ke_.p;
   ma.err = md_err_.p;
-  auto check_forces = [&] {
-    int bad = 0;
-    CU(cudaMemcpyAsync(&bad, md_err_.p, sizeof bad, cudaMemcpyDeviceToHost, st_));
-    CU(cudaStreamSynchronize(st_));
-    if (bad != 0x7f7f7f7f)
-      throw Error("run_md: non-finite force from provider 'nnmd_b200' at step " + std::to_string(bad));
+  auto check_forces = [&] {  // the flag was read back with compute_device's step flags
+    if (*h_md_err_ != 0x7f7f7f7f)
+      throw Error("run_md: non-finite force from provider 'nnmd_b200' at step " + std::to_string(*h_md_err_));
   };
+  struct Clear {
+    const MdArgs*& p;
+    ~Clear() { p = nullptr; }
+  } clear{md_check_};
   for (long step = 0; step < cfg.n_steps; ++step) {
     // forces of the current positions (replicated on every process after the all-reduce,
     // so each process integrates its own copy: no position collective is needed)
-    compute_device(n, d_pos, d_types, d_gid, box, periodic, out_.p);
     ma.step = static_cast<int>(step);
+    md_check_ = &ma;
+    compute_device(n, d_pos, d_types, d_gid, box, periodic, out_.p);
     // run_md (engine.cpp:166-176) rejects non-finite forces BEFORE integrating: the state
     // is left at the failing step
-    launch_force_check(ma, st_);
     check_forces();
     if (trace_on_) CU(cudaEventRecord(md_ev_[0], st_));
     launch_leapfrog(ma, st_);

@@ -172,6 +172,8 @@ class Context {
   int redo_depth_ = 0;
   DevBuf<int> rstat_;        // [R][kCntWords] per-rank device counts of the step
   int* h_rstat_ = nullptr;   // pinned copy
+  const MdArgs* md_check_ = nullptr;  // run_md: finite-force check folded into the step's read-back
+  int* h_md_err_ = nullptr;           // pinned
   void route_and_reduce(long n, double* d_out);
   std::vector<RankStat> stats_;
   std::vector<RankDebug> debug_;
