@@ -237,8 +237,11 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
       f *= (e + 2.0 * thickness) / e;
     }
     double est = static_cast<double>(n) / R * (f - 1.0) * 1.5 + 1024.0;
+    double loc = std::min(static_cast<double>(n), static_cast<double>(n) / R * 1.5 + 1024.0);
     if (const char* e = getenv("NNMD_GHOST_CAP")) est = atof(e);  // tests: force the overflow / redo path
+    if (const char* e = getenv("NNMD_LOCAL_CAP")) loc = atof(e);
     cap_gh_.assign(static_cast<size_t>(R), static_cast<int>(std::min(est, 27.0 * static_cast<double>(n) + 64.0)));
+    cap_loc_.assign(static_cast<size_t>(R), static_cast<int>(loc));
     cap_n_ = n;
   }
   SysArgs sys{};
@@ -297,17 +300,23 @@ void Context::compute_device(long n, const double* d_pos, const int* d_types,
     for (int r = 0; r < R; ++r) {
       if (r % opts_.world_size != opts_.world_rank) continue;
       const int* c = h_rstat_ + static_cast<size_t>(r) * kCntWords;
-      const int need = c[kCntGhExact] + (wide ? std::max(0, c[kCntCenExact] - c[kCntLoc] - c[kCntGhExact]) : 0);
-      const int cap = static_cast<int>(need * 1.25) + 1024;
+      const int cap = static_cast<int>(c[kCntGhExact] * 1.25) + 1024;
       if (cap > cap_gh_[static_cast<size_t>(r)]) {
         cap_gh_[static_cast<size_t>(r)] = cap;
+        grown = true;
+      }
+      const int capl = std::min(static_cast<int>(n), static_cast<int>(c[kCntLocExact] * 1.25) + 1024);
+      if (c[kCntLocExact] > cap_loc_[static_cast<size_t>(r)]) {
+        cap_loc_[static_cast<size_t>(r)] = capl;
         grown = true;
       }
     }
     // with several processes another process may be the one that overflowed: every process
     // redoes the step (the flags are all-reduced), growing all its capacities
-    if (!grown)
+    if (!grown) {
       for (auto& c : cap_gh_) c = static_cast<int>(c * 1.5) + 1024;
+      for (auto& c : cap_loc_) c = std::min(static_cast<int>(n), static_cast<int>(c * 1.5) + 1024);
+    }
     require(redo_depth_ < 4, "nnmd_b200: ghost capacity did not converge");
     ++redo_depth_;
     struct Reset {
@@ -494,9 +503,9 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   // and the step is redone with exact sizes (compute_device); bad input (err_[0]) raises
   // at the step's end.
   const int ngh = cap_gh_[static_cast<size_t>(rank)];  // capacities
-  const int nloc = n;
+  const int nloc = cap_loc_[static_cast<size_t>(rank)];
   const int nm = nloc + ngh;
-  launch_rank_counts(loc_off_.p, gh_off_.p, n, nm, ngh, counts_.p, err_.p + 3, st_);
+  launch_rank_counts(loc_off_.p, gh_off_.p, n, nloc, ngh, counts_.p, err_.p + 3, st_);
   m_atom_.ensure(nm + 1);
   m_shift_.ensure(nm + 1);
   m_owner_.ensure(nm + 1);

@@ -167,7 +167,7 @@ class Context {
   long route_cap_ = 0;       // entries in the local send buffers this step
   int* h_rcnt_ = nullptr;    // pinned [R][R]
   // ghost capacities per DD rank (no host read-back of counts inside a step)
-  std::vector<int> cap_gh_;
+  std::vector<int> cap_gh_, cap_loc_;
   long cap_n_ = -1;
   int redo_depth_ = 0;
   DevBuf<int> rstat_;        // [R][kCntWords] per-rank device counts of the step

@@ -170,7 +170,7 @@ __global__ void k_dd_members(SysArgs s, RankArgs r, const int* __restrict__ owne
   const int nloc = loc_off[n_atoms];
   const double p[3] = {s.pos[3 * i], s.pos[3 * i + 1], s.pos[3 * i + 2]};
   const bool mine = owner[i] == r.rank;
-  if (mine) {
+  if (mine && loc_off[i] < cap) {
     const int m = loc_off[i];
     m_atom[m] = i;
     m_shift[m] = kZeroShift;
@@ -204,23 +204,24 @@ void launch_dd_members(const SysArgs& s, const RankArgs& r, const int* owner, co
                                                   m_shift, m_pos, m_owner); count_launch();
 }
 
-__global__ void k_rank_counts(const int* __restrict__ loc_off, const int* __restrict__ gh_off, int n, int cap,
+__global__ void k_rank_counts(const int* __restrict__ loc_off, const int* __restrict__ gh_off, int n, int cap_loc,
                               int cap_gh, int* __restrict__ counts, int* __restrict__ overflow) {
   const int nloc = loc_off[n], ngh = gh_off[n];
-  const int gh = min(min(ngh, cap_gh), max(0, cap - nloc));
-  if (gh < ngh) *overflow = 1;
-  counts[kCntLoc] = nloc;
+  const int lo = min(nloc, cap_loc), gh = min(ngh, cap_gh);
+  if (lo < nloc || gh < ngh) *overflow = 1;
+  counts[kCntLoc] = lo;
   counts[kCntGh] = gh;
-  counts[kCntMem] = nloc + gh;
-  counts[kCntCen] = nloc;
+  counts[kCntMem] = lo + gh;
+  counts[kCntCen] = lo;
   counts[kCntRoute] = 0;
   counts[kCntGhExact] = ngh;
   counts[kCntCenExact] = nloc;
+  counts[kCntLocExact] = nloc;
 }
 
-void launch_rank_counts(const int* loc_off, const int* gh_off, int n_atoms, int cap_members, int cap_ghosts,
+void launch_rank_counts(const int* loc_off, const int* gh_off, int n_atoms, int cap_locals, int cap_ghosts,
                         int* counts, int* overflow, cudaStream_t st) {
-  k_rank_counts<<<1, 1, 0, st>>>(loc_off, gh_off, n_atoms, cap_members, cap_ghosts, counts, overflow); count_launch();
+  k_rank_counts<<<1, 1, 0, st>>>(loc_off, gh_off, n_atoms, cap_locals, cap_ghosts, counts, overflow); count_launch();
 }
 
 // Centres: every local; for wide_halo also the first-layer ghosts (inside the rc slab,
@@ -570,6 +571,7 @@ __global__ void __launch_bounds__(128) k_force_gather(ForceArgs a) {
   const int* list;
   int cnt;
   if (t < nloc) {
+    if (oc < 0) return;  // (only in a capacity-overflowed pass, which is redone)
     list = a.nlist + static_cast<size_t>(oc) * a.n_max;
     cnt = a.nn[oc];
   } else {

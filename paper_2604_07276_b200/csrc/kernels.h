@@ -49,12 +49,12 @@ void launch_dd_members(const SysArgs& s, const RankArgs& r, const int* owner, co
 
 // Device-resident counts of one DD rank (no host read-back inside a step):
 enum { kCntLoc = 0, kCntGh = 1, kCntCen = 2, kCntRoute = 3, kCntMem = 4, kCntGhExact = 5, kCntCenExact = 6,
-       kCntWords = 8 };
-// counts[kCntLoc] = locals, [kCntGh] = ghosts (clamped to the capacity), [kCntMem] = members,
-// [kCntCen] = locals (masked scheme; wide: set by launch_centre_compact), exact ghost count
-// in [kCntGhExact]; *overflow = 1 when the ghosts exceed cap_ghosts (or the members
-// cap_members).
-void launch_rank_counts(const int* loc_off, const int* gh_off, int n_atoms, int cap_members, int cap_ghosts,
+       kCntLocExact = 7, kCntWords = 8 };
+// counts[kCntLoc] = locals, [kCntGh] = ghosts (each clamped to its capacity), [kCntMem] =
+// members, [kCntCen] = locals (masked scheme; wide: set by launch_centre_compact), the exact
+// counts in [kCntLocExact], [kCntGhExact]; *overflow = 1 when a capacity is exceeded (the
+// step's outputs are then discarded and it is redone: kernels only need to stay in bounds).
+void launch_rank_counts(const int* loc_off, const int* gh_off, int n_atoms, int cap_locals, int cap_ghosts,
                         int* counts, int* overflow, cudaStream_t st);
 // centre flags over members (locals always; first-layer ghosts when wide)
 void launch_centre_flags(const RankArgs& r, const int* counts /*[nloc, ngh]*/, const double* m_pos,

@@ -322,21 +322,22 @@ def test_virial_is_strain_derivative_on_gpu():
 
 
 @pytest.mark.parametrize("scheme", [nb.MASKED_REDUCTION, nb.WIDE_HALO])
-def test_ghost_capacity_overflow_redo(monkeypatch, scheme):
-    """The DD build has no host read-back: buffers are sized by ghost capacities and an
-    overflow is flagged on the device, then the step is redone with grown capacities.
-    A capacity of 16 ghosts forces that path; the result must equal, bit for bit, a run
-    whose first estimate fits, and the golden dd_evaluate result."""
+@pytest.mark.parametrize("which", ["NNMD_GHOST_CAP", "NNMD_LOCAL_CAP"])
+def test_ghost_capacity_overflow_redo(monkeypatch, scheme, which):
+    """The DD build has no host read-back: buffers are sized by per-rank local and ghost
+    capacities and an overflow is flagged on the device, then the step is redone with
+    grown capacities.  A capacity of 16 forces that path; the result must equal, bit for
+    bit, a run whose first estimate fits."""
     g = load_golden("dd_case_0")
     m = nb.init_model(nb.test_spec(float(g["rc"])), int(g["model_seed"]))
     ref = nb.DeviceEvaluator(m, n_ranks=4, scheme=scheme).compute(g["pos"], g["species"], g["box"])
-    monkeypatch.setenv("NNMD_GHOST_CAP", "16")
+    monkeypatch.setenv(which, "16")
     ev = nb.DeviceEvaluator(m, n_ranks=4, scheme=scheme)
     r = ev.compute(g["pos"], g["species"], g["box"])
     for k in ("forces", "virial", "atom_energy"):
         assert np.array_equal(r[k], ref[k]), k
     assert r["energy"] == ref["energy"]
     st = [ev.rank_stats(q) for q in range(4)]
-    assert all(s["ghosts"] > 16 for s in st)
+    assert all(s["ghosts"] > 16 and s["locals"] > 16 for s in st)
     r2 = ev.compute(g["pos"], g["species"], g["box"])  # grown capacities are kept
     assert np.array_equal(r2["forces"], ref["forces"])
