@@ -809,7 +809,7 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   fa.dD = dD_.p;
   fa.mode = dp.mode;
   fa.n_sm = n_sm_;
-  fitws_.ensure(fit_workspace_floats(ncen, 256, n_sm_));  // split-K only for layers with N <= 256
+  fitws_.ensure(fit_workspace_floats(ncen, 256));  // split-K only for layers with N <= 256
   fa.ws = fitws_.p;
   tic("fit");
   launch_fit(fa, st_);
@@ -854,7 +854,6 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   fo.rn = wide ? nullptr : rn_.p;
   fo.counts = counts_.p;
   fo.wide = wide;
-  fo.nloc = nloc;
   fo.n_targets = wide ? nloc : nm;
   fo.g = g_.p;
   fo.fmem = fmem_.p;

@@ -263,11 +263,11 @@ __global__ void k_centre_compact(const int* __restrict__ flag, const int* __rest
   }
 }
 
-void launch_centre_compact(const int* flag, const int* off, const int* counts, int n_members_cap, int wide,
+void launch_centre_compact(const int* flag, const int* off, int* counts, int n_members_cap, int wide,
                            int cap_centres, int* cen_member, int* cidx, int* overflow, cudaStream_t st) {
   if (n_members_cap == 0) return;
-  k_centre_compact<<<(n_members_cap + 255) / 256, 256, 0, st>>>(flag, off, const_cast<int*>(counts), wide,
-                                                                cap_centres, cen_member, cidx, overflow);
+  k_centre_compact<<<(n_members_cap + 255) / 256, 256, 0, st>>>(flag, off, counts, wide, cap_centres, cen_member,
+                                                                cidx, overflow);
   count_launch();
 }
 
@@ -785,7 +785,7 @@ void launch_finalize(const double* red, int n_ranks, long n_atoms, double* out, 
 // Multi-centre tiles (rc = 4: n <= 64, ~27 rows per centre): groups of four consecutive
 // centres become one 128-row unit when their rows fit, else two pairs (always fit).
 // ----------------------------------------------------------------------------------
-__device__ __forceinline__ int pack_group_units(const int* nn, int n_centres, int g) {  // g < groups
+__device__ __forceinline__ int pack_group_units(const int* nn, int n_centres, int g) {
   const int c0 = 4 * g, c1 = min(n_centres, c0 + 4);
   int rows = 0;
   for (int c = c0; c < c1; ++c) rows += nn[c];

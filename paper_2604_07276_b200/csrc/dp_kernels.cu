@@ -1475,7 +1475,7 @@ static void fit_gemm_tb(bool tb, int M, const int* M_live, int N, int K, const f
   else fit_gemm<false, MODE>(M, M_live, N, K, A, B, ldb, C, bias, Y, epi, st, ws, n_sm);
 }
 
-size_t fit_workspace_floats(int n_centres, int width, int) {
+size_t fit_workspace_floats(int n_centres, int width) {
   return static_cast<size_t>(kFitSplit) * n_centres * width + 4;
 }
 

@@ -61,7 +61,7 @@ void launch_centre_flags(const RankArgs& r, const int* counts /*[nloc, ngh]*/, c
                          int n_members_cap, int* flag, cudaStream_t st);
 // over counts[kCntMem] members (grid: n_members_cap); wide_halo also sets counts[kCntCen]
 // (clamped to cap_centres, *overflow = 1 beyond it)
-void launch_centre_compact(const int* flag, const int* off, const int* counts, int n_members_cap, int wide,
+void launch_centre_compact(const int* flag, const int* off, int* counts, int n_members_cap, int wide,
                            int cap_centres, int* cen_member, int* cidx, int* overflow, cudaStream_t st);
 
 // ---------------------------------------------------------------- cells / neighbours -
@@ -134,7 +134,6 @@ struct ForceArgs {
   const int* cidx;       // member -> centre index, -1 if not a centre
   const int* rlist;      // ghost reverse lists (masked), [n_ghost][n_max]
   const int* rn;
-  int nloc;              // (unused: device counts)
   int n_targets;         // capacity (grid); live: masked all members, wide locals
   const double* g;       // [centre][n_max][3] row gradients de/dd_k
   double* fmem;          // [member][3] force partial
@@ -306,12 +305,12 @@ struct FitArgs {
   double* e;                 // [n_centres]
   float* dD;
   int mode;
-  int n_sm;                  // SMs of the device (split-K sizing)
+  int n_sm;                  // SMs of the device
   float* ws;                 // split-K partial sums, fit_workspace_floats(...) floats
 };
 // Split-K workspace of the fitting net's K = M * mr layer (small centre counts: one row
 // tile per 128 centres cannot fill the GPU, so K is split and the partials summed in order)
-size_t fit_workspace_floats(int n_centres, int width, int n_sm);
+size_t fit_workspace_floats(int n_centres, int width);
 void launch_fit(const FitArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------- MD loop -------------
