@@ -13,6 +13,8 @@
 // One host read-back per rank (the DD-build counts, to size the rest of the step).
 #include "context.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <chrono>
 #include <fstream>
@@ -170,11 +172,13 @@ void Context::tic(const char* name) {
   pool_used_ += 2;
   CU(cudaEventRecord(t.a, st_));
   timers_.push_back(t);
+  nvtxRangePushA(name);  // the same phase names for nsys / ncu NVTX filtering
 }
 
 void Context::toc() {
   check_launch(timers_.back().name.c_str());
   CU(cudaEventRecord(timers_.back().b, st_));
+  nvtxRangePop();
 }
 
 void Context::collect_times() {
