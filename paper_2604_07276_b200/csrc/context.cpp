@@ -803,7 +803,9 @@ void Context::run_rank(int rank, const SysArgs& sys, const int dims[3], double t
   for (int l = 0; l < dp.n_fit; ++l) {
     fa.fw[l] = dp.fw[l];
     fa.fb[l] = dp.fb[l];
+    fa.fwT[l] = W + wh_.fwT[static_cast<size_t>(l)];
   }
+  fa.flags = flags;
   fa.n_centres = ncen;
   fa.n_centres_dev = counts_.p + kCntCen;
   fa.D = D_.p;

@@ -1504,9 +1504,20 @@ __global__ void k_fill_rows(int nc, const int* __restrict__ nc_live, int H, cons
   out[i] = w[i % H];
 }
 
+void launch_fit_out(const FitArgs& a, float* delta, cudaStream_t st) {
+  const int nc = a.n_centres, L = a.n_fit, H = a.fdims[L - 1];
+  k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, a.n_centres_dev, H, a.Y[L - 2], a.fw[L - 1], a.fb[L - 1],
+                                                   a.e, delta);
+  count_launch();
+}
+
 void launch_fit(const FitArgs& a, cudaStream_t st) {
   const int nc = a.n_centres;
   if (nc == 0) return;
+  if (!(a.flags & 32) && fit_tma_supported(a)) {
+    launch_fit_tma(a, st);
+    return;
+  }
   const int L = a.n_fit;
   auto gemm = [&](bool tb, int N, int K, const float* A, const float* B, int ldb, float* C,
                   const float* bias, const float* Y, int mode) {

@@ -1,0 +1,127 @@
+// Fitting net (dp_core.hpp:386-391 forward, 408-414 backward) on the TMA-fed tcgen05 GEMM
+// engine (tma_gemm.cuh): every 128 x 16 operand tile arrives by cp.async.bulk.tensor into a
+// four-stage shared-memory ring, warps 1-7 form the 3xTF32 low parts while warp 0 issues
+// the MMAs, and warps 8-11 promote each 128-wide K group of the accumulator in FP32 (the
+// tensor core's own accumulation truncates).  These are plain dense GEMMs over all
+// centres (M = centres, K = 4096 / 240), the place where 128-row TMA boxes do not
+// over-read; the per-centre kernels keep the register-staged engine (tc_gemm.cuh), whose
+// 128-row operands would over-read a ~90-row centre by 1.4x.
+//
+// Persistent: one CTA per SM walks the 128 x 128 output tiles row tile by row tile, so
+// neighbouring CTAs share A rows in L2.  B operands are K-major: the forward reads the
+// weights as stored ([out][in]), the backward their transposes ([in][out], built once per
+// context).  Tensor maps are encoded per call (the buffers they point at may move).
+#include <cuda.h>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tma_gemm.cuh"
+#include "tmap.h"
+
+namespace nb {
+
+enum { FEPI_STORE = 0, FEPI_TANH_BIAS = 1, FEPI_DTANH = 2 };
+constexpr int kFitPromote = 8;  // chunks of 16 per FP32 promotion group = 128 of K
+
+struct FitTmaArgs {
+  CUtensorMap ma, mb;  // A [M][K], B [N][K] (K-major)
+  int M, N, K;         // M: row capacity
+  const int* M_live;   // live rows (NULL: M)
+  float* C;            // [M][N]
+  const float* bias;   // [N] (FEPI_TANH_BIAS)
+  const float* Y;      // [M][N] tanh activations (FEPI_DTANH)
+  int epi;
+};
+
+template <int NPASS>
+__global__ void __launch_bounds__(tg::kPromoThreads, 1) k_fit_tma(const __grid_constant__ FitTmaArgs a) {
+  extern __shared__ __align__(1024) unsigned char fit_raw[];
+  uint8_t* ring = fit_raw + ((1024 - (tc::smem_u32(fit_raw) & 1023)) & 1023);
+  tg::Ctl* ctl = reinterpret_cast<tg::Ctl*>(ring + tg::kRingBytes);
+  const int Mv = a.M_live ? min(a.M, *a.M_live) : a.M;
+  const int tn = (a.N + 127) / 128, tm = (Mv + 127) / 128;
+  if (static_cast<int>(blockIdx.x) >= tm * tn) return;
+  tg::Ring rg;
+  tg::init(rg, ring, ctl, 512);
+  for (int t = blockIdx.x; t < tm * tn; t += gridDim.x) {
+    const int m0 = (t / tn) * 128, n0 = (t % tn) * 128;
+    const int Ms = min(128, Mv - m0), Ns = min(128, a.N - n0);
+    float* __restrict__ C = a.C;
+    const int N = a.N, epi = a.epi;
+    const float* __restrict__ bias = a.bias;
+    const float* __restrict__ Y = a.Y;
+    tg::gemm1<NPASS, 1, kFitPromote>(rg, Ms, Ns, a.K, tg::op(&a.ma, 0, m0, 0, tg::kOpBytes),
+                                     tg::op(&a.mb, 0, n0, 0, tg::kOpBytes), [&](int r, int c, auto v) {
+                                       const size_t o = static_cast<size_t>(m0 + r) * N + n0 + c;
+                                       if (epi == FEPI_TANH_BIAS) v = vtanh(v + vld(&bias[n0 + c], v));
+                                       else if (epi == FEPI_DTANH) v = v * vdtanh(vld(&Y[o], v));
+                                       vst(&C[o], v);
+                                     });
+  }
+  tg::finish(rg);
+}
+
+static constexpr size_t fit_tma_smem() { return tg::kRingBytes + sizeof(tg::Ctl) + 1024; }
+
+// C[M][N] = epi(A[M][K] B[N][K]^T) over the live rows
+static void fit_tma(int npass, int n_sm, int M, const int* M_live, int N, int K, const float* A, const float* B,
+                    float* C, const float* bias, const float* Y, int epi, cudaStream_t st) {
+  FitTmaArgs a;
+  make_tmap(&a.ma, A, M, K, K, 0, 128);
+  make_tmap(&a.mb, B, N, K, K, 0, 128);
+  a.M = M;
+  a.M_live = M_live;
+  a.N = N;
+  a.K = K;
+  a.C = C;
+  a.bias = bias;
+  a.Y = Y;
+  a.epi = epi;
+  const int tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  const int grid = tiles < n_sm ? tiles : n_sm;
+  const size_t smem = fit_tma_smem();
+  if (npass == 3) {
+    ensure_smem_attr(reinterpret_cast<const void*>(k_fit_tma<3>), smem);
+    k_fit_tma<3><<<grid, tg::kPromoThreads, smem, st>>>(a);
+  } else {
+    ensure_smem_attr(reinterpret_cast<const void*>(k_fit_tma<1>), smem);
+    k_fit_tma<1><<<grid, tg::kPromoThreads, smem, st>>>(a);
+  }
+  count_launch();
+}
+
+// tcgen05 modes, at least one hidden layer, every GEMM K (= fdims[0 .. n_fit-1]) a multiple
+// of the 16-wide TMA K slice
+bool fit_tma_supported(const FitArgs& a) {
+  if (a.mode == 0 || a.n_fit < 2 || !a.fwT[0]) return false;
+  for (int l = 0; l < a.n_fit; ++l)
+    if (a.fdims[l] % 16) return false;
+  return true;
+}
+
+void launch_fit_tma(const FitArgs& a, cudaStream_t st) {
+  const int nc = a.n_centres;
+  if (nc == 0) return;
+  const int L = a.n_fit, np = a.mode == 1 ? 3 : 1;
+  const int* ml = a.n_centres_dev;
+  const float* x = a.D;
+  for (int l = 0; l + 1 < L; ++l) {
+    fit_tma(np, a.n_sm, nc, ml, a.fdims[l + 1], a.fdims[l], x, a.fw[l], a.Y[l], a.fb[l], nullptr, FEPI_TANH_BIAS,
+            st);
+    x = a.Y[l];
+  }
+  float* dcur = a.delta[0];
+  float* dnxt = a.delta[1];
+  launch_fit_out(a, dcur, st);
+  // delta_{l-1} = (delta_l W_l) o (1 - Y_{l-1}^2);  dD = delta_0 W_0   (B = W_l^T, K-major)
+  for (int l = L - 2; l >= 1; --l) {
+    fit_tma(np, a.n_sm, nc, ml, a.fdims[l], a.fdims[l + 1], dcur, a.fwT[l], dnxt, nullptr, a.Y[l - 1], FEPI_DTANH,
+            st);
+    float* t = dcur;
+    dcur = dnxt;
+    dnxt = t;
+  }
+  fit_tma(np, a.n_sm, nc, ml, a.fdims[0], a.fdims[1], dcur, a.fwT[0], a.dD, nullptr, nullptr, FEPI_STORE, st);
+}
+
+}  // namespace nb

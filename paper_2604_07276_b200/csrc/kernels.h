@@ -307,7 +307,14 @@ struct FitArgs {
   int mode;
   int n_sm;                  // SMs of the device
   float* ws;                 // split-K partial sums, fit_workspace_floats(...) floats
+  const float* fwT[kMaxLayers];  // W_l^T ([in][out]): K-major B operands of the backward
+  int flags;                 // NNMD_FLAGS (bit 5: register-staged fit GEMMs instead of TMA)
 };
+// e[c] = b + w . Y_{L-2}[c]; delta = w (1 - Y^2)
+void launch_fit_out(const FitArgs& a, float* delta, cudaStream_t st);
+// The fitting net on the TMA-fed engine (fit_kernels.cu), when fit_tma_supported(a)
+bool fit_tma_supported(const FitArgs& a);
+void launch_fit_tma(const FitArgs& a, cudaStream_t st);
 // Split-K workspace of the fitting net's K = M * mr layer (small centre counts: one row
 // tile per 128 centres cannot fill the GPU, so K is split and the partials summed in order)
 size_t fit_workspace_floats(int n_centres, int width);

@@ -278,6 +278,10 @@ DeviceWeightsHost fold_weights(const Model& m) {
     for (size_t i = 0; i < ly.w.size(); ++i) d.blob[d.fw.back() + i] = static_cast<float>(ly.w[i]);
     d.fb.push_back(alloc(ly.b.size()));
     for (size_t i = 0; i < ly.b.size(); ++i) d.blob[d.fb.back() + i] = static_cast<float>(ly.b[i]);
+    d.fwT.push_back(alloc(ly.w.size()));
+    for (int o = 0; o < ly.nout; ++o)
+      for (int i = 0; i < ly.nin; ++i)
+        d.blob[d.fwT.back() + static_cast<size_t>(i) * ly.nout + o] = static_cast<float>(ly.w[static_cast<size_t>(o) * ly.nin + i]);
     d.fdims.push_back(ly.nout);
   }
   alloc(4);

@@ -60,7 +60,8 @@ struct DeviceWeightsHost {
   std::vector<long> ew, eb;        // embed layers 1.. (index 0 unused)
   std::vector<int> edims;          // widths: edims[0] = E0 (layer-0 out), ... edims.back() = M
   std::vector<long> ab;            // per attention layer, M x 2M
-  std::vector<long> fw, fb;        // fit layers
+  std::vector<long> fw, fb;        // fit layers ([out][in] weights, biases)
+  std::vector<long> fwT;           // fit weights transposed ([in][out]): backward GEMM B operands
   std::vector<int> fdims;          // fit widths: fdims[0] = M*mr, ..., fdims.back() = 1
 };
 
