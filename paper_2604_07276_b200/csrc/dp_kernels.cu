@@ -1504,6 +1504,15 @@ __global__ void k_fill_rows(int nc, const int* __restrict__ nc_live, int H, cons
   out[i] = w[i % H];
 }
 
+int fit_split_k(int K) { return fit_split(K); }
+
+void launch_fit_splitk_sum(int M, const int* M_live, int N, int S, const float* P, float* C, const float* bias,
+                           const float* Y, int epi, cudaStream_t st) {
+  const size_t MN = static_cast<size_t>(M) * N;
+  k_fit_splitk_sum<<<static_cast<int>((MN + 255) / 256), 256, 0, st>>>(M, M_live, N, S, P, C, bias, Y, epi);
+  count_launch();
+}
+
 void launch_fit_out(const FitArgs& a, float* delta, cudaStream_t st) {
   const int nc = a.n_centres, L = a.n_fit, H = a.fdims[L - 1];
   k_fit_out<<<(nc * 32 + 255) / 256, 256, 0, st>>>(nc, a.n_centres_dev, H, a.Y[L - 2], a.fw[L - 1], a.fb[L - 1],

@@ -31,6 +31,7 @@ struct FitTmaArgs {
   const float* bias;   // [N] (FEPI_TANH_BIAS)
   const float* Y;      // [M][N] tanh activations (FEPI_DTANH)
   int epi;
+  int S;               // K slices (split-K): raw partial tiles into C's slice z, epilogue later
 };
 
 template <int NPASS>
@@ -40,18 +41,21 @@ __global__ void __launch_bounds__(tg::kPromoThreads, 1) k_fit_tma(const __grid_c
   tg::Ctl* ctl = reinterpret_cast<tg::Ctl*>(ring + tg::kRingBytes);
   const int Mv = a.M_live ? min(a.M, *a.M_live) : a.M;
   const int tn = (a.N + 127) / 128, tm = (Mv + 127) / 128;
-  if (static_cast<int>(blockIdx.x) >= tm * tn) return;
+  const int items = tm * tn * a.S;  // (K slice, row tile, column tile)
+  if (static_cast<int>(blockIdx.x) >= items) return;
   tg::Ring rg;
   tg::init(rg, ring, ctl, 512);
-  for (int t = blockIdx.x; t < tm * tn; t += gridDim.x) {
+  const int Kc = a.K / a.S;
+  for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    const int z = w / (tm * tn), t = w - z * tm * tn;
     const int m0 = (t / tn) * 128, n0 = (t % tn) * 128;
     const int Ms = min(128, Mv - m0), Ns = min(128, a.N - n0);
-    float* __restrict__ C = a.C;
-    const int N = a.N, epi = a.epi;
+    float* __restrict__ C = a.C + static_cast<size_t>(z) * a.M * a.N;
+    const int N = a.N, epi = a.S > 1 ? FEPI_STORE : a.epi;
     const float* __restrict__ bias = a.bias;
     const float* __restrict__ Y = a.Y;
-    tg::gemm1<NPASS, 1, kFitPromote>(rg, Ms, Ns, a.K, tg::op(&a.ma, 0, m0, 0, tg::kOpBytes),
-                                     tg::op(&a.mb, 0, n0, 0, tg::kOpBytes), [&](int r, int c, auto v) {
+    tg::gemm1<NPASS, 1, kFitPromote>(rg, Ms, Ns, Kc, tg::op(&a.ma, 0, m0, z * Kc, tg::kOpBytes),
+                                     tg::op(&a.mb, 0, n0, z * Kc, tg::kOpBytes), [&](int r, int c, auto v) {
                                        const size_t o = static_cast<size_t>(m0 + r) * N + n0 + c;
                                        if (epi == FEPI_TANH_BIAS) v = vtanh(v + vld(&bias[n0 + c], v));
                                        else if (epi == FEPI_DTANH) v = v * vdtanh(vld(&Y[o], v));
@@ -63,9 +67,10 @@ __global__ void __launch_bounds__(tg::kPromoThreads, 1) k_fit_tma(const __grid_c
 
 static constexpr size_t fit_tma_smem() { return tg::kRingBytes + sizeof(tg::Ctl) + 1024; }
 
-// C[M][N] = epi(A[M][K] B[N][K]^T) over the live rows
+// C[M][N] = epi(A[M][K] B[N][K]^T) over the live rows; with K split (fit_split_k, needs the
+// workspace ws of S * M * N floats) the slices go to ws and a fixed-order sum applies epi
 static void fit_tma(int npass, int n_sm, int M, const int* M_live, int N, int K, const float* A, const float* B,
-                    float* C, const float* bias, const float* Y, int epi, cudaStream_t st) {
+                    float* C, const float* bias, const float* Y, int epi, float* ws, cudaStream_t st) {
   FitTmaArgs a;
   make_tmap(&a.ma, A, M, K, K, 0, 128);
   make_tmap(&a.mb, B, N, K, K, 0, 128);
@@ -77,7 +82,9 @@ static void fit_tma(int npass, int n_sm, int M, const int* M_live, int N, int K,
   a.bias = bias;
   a.Y = Y;
   a.epi = epi;
-  const int tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  a.S = ws ? fit_split_k(K) : 1;
+  if (a.S > 1) a.C = ws;
+  const int tiles = ((M + 127) / 128) * ((N + 127) / 128) * a.S;
   const int grid = tiles < n_sm ? tiles : n_sm;
   const size_t smem = fit_tma_smem();
   if (npass == 3) {
@@ -88,6 +95,7 @@ static void fit_tma(int npass, int n_sm, int M, const int* M_live, int N, int K,
     k_fit_tma<1><<<grid, tg::kPromoThreads, smem, st>>>(a);
   }
   count_launch();
+  if (a.S > 1) launch_fit_splitk_sum(M, M_live, N, a.S, ws, C, bias, Y, epi, st);
 }
 
 // tcgen05 modes, at least one hidden layer, every GEMM K (= fdims[0 .. n_fit-1]) a multiple
@@ -107,7 +115,7 @@ void launch_fit_tma(const FitArgs& a, cudaStream_t st) {
   const float* x = a.D;
   for (int l = 0; l + 1 < L; ++l) {
     fit_tma(np, a.n_sm, nc, ml, a.fdims[l + 1], a.fdims[l], x, a.fw[l], a.Y[l], a.fb[l], nullptr, FEPI_TANH_BIAS,
-            st);
+            a.fdims[l + 1] <= 256 ? a.ws : nullptr, st);
     x = a.Y[l];
   }
   float* dcur = a.delta[0];
@@ -116,12 +124,12 @@ void launch_fit_tma(const FitArgs& a, cudaStream_t st) {
   // delta_{l-1} = (delta_l W_l) o (1 - Y_{l-1}^2);  dD = delta_0 W_0   (B = W_l^T, K-major)
   for (int l = L - 2; l >= 1; --l) {
     fit_tma(np, a.n_sm, nc, ml, a.fdims[l], a.fdims[l + 1], dcur, a.fwT[l], dnxt, nullptr, a.Y[l - 1], FEPI_DTANH,
-            st);
+            nullptr, st);
     float* t = dcur;
     dcur = dnxt;
     dnxt = t;
   }
-  fit_tma(np, a.n_sm, nc, ml, a.fdims[0], a.fdims[1], dcur, a.fwT[0], a.dD, nullptr, nullptr, FEPI_STORE, st);
+  fit_tma(np, a.n_sm, nc, ml, a.fdims[0], a.fdims[1], dcur, a.fwT[0], a.dD, nullptr, nullptr, FEPI_STORE, nullptr, st);
 }
 
 }  // namespace nb

@@ -312,6 +312,12 @@ struct FitArgs {
 };
 // e[c] = b + w . Y_{L-2}[c]; delta = w (1 - Y^2)
 void launch_fit_out(const FitArgs& a, float* delta, cudaStream_t st);
+// Split-K of the wide fitting layer: slice count for a K (K only: rank-count invariant), and
+// the fixed-order sum of the S raw slices P[z][M][N] with the layer's epilogue (epi: 0
+// store, 1 tanh(x + bias), 2 x (1 - Y^2))
+int fit_split_k(int K);
+void launch_fit_splitk_sum(int M, const int* M_live, int N, int S, const float* P, float* C, const float* bias,
+                           const float* Y, int epi, cudaStream_t st);
 // The fitting net on the TMA-fed engine (fit_kernels.cu), when fit_tma_supported(a)
 bool fit_tma_supported(const FitArgs& a);
 void launch_fit_tma(const FitArgs& a, cudaStream_t st);
