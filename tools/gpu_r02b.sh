@@ -26,7 +26,7 @@ if [ -z "${NO_NCU:-}" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/${T}_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"k_neighbors|k_force_gather|k_route|k_merge|k_energy_virial|k_fit_gemm|k_fit_splitk|k_dd_members|k_cell_fill|k_finalize" -c 24 \
+  -k regex:"k_neighbors|k_force_gather|k_route|k_merge|k_energy_virial|k_fit_tma|k_fit_out|k_fit_splitk|k_dd_members|k_cell_fill|k_finalize" -c 26 \
   -o gpurun_out/${T}_hbm python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/${T}_ncu_hbm.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_centre_(forward|backward)" -c 2 \
   -o gpurun_out/${T}_centre python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/${T}_ncu_centre.log 2>&1
