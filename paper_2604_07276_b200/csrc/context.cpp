@@ -436,18 +436,56 @@ void Context::route_and_reduce(long n, double* d_out) {
   inc_cnt_.ensure(static_cast<size_t>(n) + 1);
   inc_off_.ensure(static_cast<size_t>(n) + 1);
   seg_.ensure(2 * static_cast<size_t>(R) * R + 1);
-  inc_.ensure(static_cast<size_t>(capacity) + 1);
-  CU(cudaMemsetAsync(inc_cnt_.p, 0, (static_cast<size_t>(n) + 1) * sizeof(int), st_));
   ma.seg = seg_.p;
   ma.inc_cnt = inc_cnt_.p;
   ma.inc_off = inc_off_.p;
-  ma.inc = inc_.p;
-  ma.capacity = static_cast<int>(capacity);
   ma.owner = owner_.p;
   ma.fown = fown_.p;
   ma.f_out = red_.p + 10 * static_cast<size_t>(R);
+  auto merge = [&](MergeArgs& a, long cap) {
+    inc_.ensure(static_cast<size_t>(cap) + 1);
+    CU(cudaMemsetAsync(inc_cnt_.p, 0, (static_cast<size_t>(n) + 1) * sizeof(int), st_));
+    a.inc = inc_.p;
+    a.capacity = static_cast<int>(cap);
+    launch_route_merge(a, st_);
+  };
   tic("route_merge");
-  launch_route_merge(ma, st_);
+  // Test hook (NNMD_EMULATE_WORLD=W, one process): run the several-process route as W
+  // processes would -- the plan of every emulated process, its receives as device copies
+  // from the senders' grouped buffers, and its merge over the atoms it owns -- so the
+  // multi-process layout (receive buffers, remote segment offsets) is checked on one GPU
+  // against the single-process result (tests/test_gpu_parity.py).
+  static const int emulate = getenv("NNMD_EMULATE_WORLD") ? atoi(getenv("NNMD_EMULATE_WORLD")) : 0;
+  if (emulate > 1 && !multi && masked && ws == 1) {
+    CU(cudaMemcpyAsync(h_rcnt_, rcnt_.p, static_cast<size_t>(R) * R * sizeof(int), cudaMemcpyDeviceToHost, st_));
+    CU(cudaStreamSynchronize(st_));
+    for (int fw = 0; fw < emulate; ++fw) {
+      MergeArgs me = ma;
+      me.world_size = emulate;
+      me.world_rank = fw;
+      long cap = route_cap_;
+      for (int s2 = 0; s2 < R; ++s2) {
+        me.src_base[s2] = route_buf_[s2].p;
+        if (s2 % emulate == fw) continue;
+        long tot = 0;
+        for (int o = 0; o < R; ++o)
+          if (o % emulate == fw) tot += h_rcnt_[s2 * R + o];
+        recv_buf_[s2].ensure(static_cast<size_t>(tot) + 1);
+        me.src_base[s2] = recv_buf_[s2].p;
+        cap += tot;
+      }
+      for (const RouteOp& op : route_schedule(R, emulate, fw, h_rcnt_)) {
+        if (op.kind != 1) continue;
+        long soff = 0;  // the sender's group offset (its own send op's offset)
+        for (int o = 0; o < op.dst; ++o) soff += h_rcnt_[op.src * R + o];
+        CU(cudaMemcpyAsync(recv_buf_[op.src].p + op.offset, route_buf_[op.src].p + soff,
+                           static_cast<size_t>(op.count) * sizeof(RouteEntry), cudaMemcpyDeviceToDevice, st_));
+      }
+      merge(me, cap);
+    }
+  } else {
+    merge(ma, capacity);
+  }
   toc();
   if (use_nccl_) {
     // collective 2 (reduce_forces, decomp.cpp:188-204): the result rows, forces and atom

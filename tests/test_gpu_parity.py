@@ -341,3 +341,37 @@ def test_ghost_capacity_overflow_redo(monkeypatch, scheme, which):
     assert all(s["ghosts"] > 16 and s["locals"] > 16 for s in st)
     r2 = ev.compute(g["pos"], g["species"], g["box"])  # grown capacities are kept
     assert np.array_equal(r2["forces"], ref["forces"])
+
+
+def test_route_as_several_processes(monkeypatch):
+    """The point-to-point ghost-force route as W processes would run it (NNMD_EMULATE_WORLD:
+    each emulated process's plan, its receives as device copies into the receive buffers,
+    its merge over the atoms it owns) must give the single-process result bit for bit --
+    this checks the receive-buffer layout and the remote segment offsets of the merge on
+    one GPU; only the NCCL transport itself is left to a multi-GPU box."""
+    import subprocess, sys, json, os
+    g = "dd_case_0"
+    code = (
+        "import sys, json, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_2604_07276_b200 as nb\nfrom conftest import load_golden\n"
+        "g = load_golden(%r)\n"
+        "m = nb.init_model(nb.test_spec(float(g['rc'])), int(g['model_seed']))\n"
+        "out = {}\n"
+        "for R in (2, 4, 8):\n"
+        "    r = nb.DeviceEvaluator(m, n_ranks=R).compute(g['pos'], g['species'], g['box'])\n"
+        "    out[R] = [r['energy'], r['forces'].tolist(), r['atom_energy'].tolist()]\n"
+        "print(json.dumps(out))\n"
+    ) % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)), g)
+    def run(env):
+        e = dict(os.environ)
+        e.update(env)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        return json.loads(p.stdout.strip().splitlines()[-1])
+    base = run({})
+    for w in ("2", "3"):
+        emu = run({"NNMD_EMULATE_WORLD": w})
+        for R in base:
+            assert emu[R][0] == base[R][0]
+            assert emu[R][1] == base[R][1]
+            assert emu[R][2] == base[R][2]
