@@ -97,6 +97,7 @@ std::vector<int> partition_ranks(const double L[3], int R, double min_edge) {
 Context::Context(const Model& m, const nnmd_b200_opts& o) : model_(m), opts_(o) {
   model_.validate();
   require(o.n_ranks >= 1, "nnmd_b200: n_ranks must be >= 1");
+  require(m.n_max >= 1 && m.n_max < 1024, "nnmd_b200: n_max must be below 1024");
   require(o.scheme == NNMD_MASKED_REDUCTION || o.scheme == NNMD_WIDE_HALO, "nnmd_b200: bad scheme");
   require(o.precision == NNMD_PREC_FP32 || o.precision == NNMD_PREC_TF32 || o.precision == NNMD_PREC_FP32_SIMT,
           "nnmd_b200: unsupported precision");

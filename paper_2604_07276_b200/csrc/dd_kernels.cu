@@ -389,6 +389,17 @@ __device__ __forceinline__ double env_row(const NbrArgs& a, int li, int k, const
   return sw * sw;
 }
 
+// sigma = sum_k s_k^2 in canonical row order (lane l adds rows l, l + 32, ..., then a fixed
+// warp tree): independent of the order candidates reached the list, so bit-reproducible
+// (the cell lists are filled with atomics) and equal to a row-by-row evaluation.
+__device__ __forceinline__ void env_sigma(const NbrArgs& a, int li, int cnt, const double* sr) {
+  const int lane = threadIdx.x & 31;
+  double sig = 0.0;
+  for (int k = lane; k < cnt; k += 32) sig += sr[k];
+  sig = warp_sum(sig);
+  if (lane == 0) a.sig[li] = sig;
+}
+
 // ENV: centre lists, which also write their environment rows (env_row).
 template <bool ENV>
 __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap) {
@@ -504,30 +515,41 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
         rank[u] = r;
       }
     }
-    double sig = 0.0;
+    double s2[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u)
       if (lane + 32 * u < cnt) {
         const NbrEntry me = buf[lane + 32 * u];
         out[rank[u]] = a.cell_members[me.j];
-        if constexpr (ENV) sig += env_row(a, li, rank[u], me, pc, csh);
+        if constexpr (ENV) s2[u] = env_row(a, li, rank[u], me, pc, csh);
       }
     if constexpr (ENV) {
-      sig = warp_sum(sig);  // lane partials in a fixed order, then a fixed warp tree
-      if (lane == 0) a.sig[li] = sig;
+      __syncwarp();  // every entry consumed: buf becomes the rank-ordered s^2 array
+      double* sr = reinterpret_cast<double*>(buf);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (lane + 32 * u < cnt) sr[rank[u]] = s2[u];
+      __syncwarp();
+      env_sigma(a, li, cnt, sr);
     }
   } else {
-    double sig = 0.0;
-    for (int i = lane; i < cnt; i += 32) {
+    constexpr int kMaxPer = 32;  // n_max < 1024 (context checks)
+    double s2[kMaxPer];
+    int rk[kMaxPer];
+    for (int i = lane, u = 0; i < cnt; i += 32, ++u) {
       const NbrEntry me = buf[i];
       int rank = 0;
       for (int j = 0; j < cnt; ++j) rank += full_less(a, buf[j], me, pc, csh);
       out[rank] = a.cell_members[me.j];
-      if constexpr (ENV) sig += env_row(a, li, rank, me, pc, csh);
+      rk[u] = rank;
+      if constexpr (ENV) s2[u] = env_row(a, li, rank, me, pc, csh);
     }
     if constexpr (ENV) {
-      sig = warp_sum(sig);
-      if (lane == 0) a.sig[li] = sig;
+      __syncwarp();
+      double* sr = reinterpret_cast<double*>(buf);
+      for (int i = lane, u = 0; i < cnt; i += 32, ++u) sr[rk[u]] = s2[u];
+      __syncwarp();
+      env_sigma(a, li, cnt, sr);
     }
   }
 }
