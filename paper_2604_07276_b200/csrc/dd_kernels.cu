@@ -420,47 +420,57 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
   const int cand_limit = a.cand_limit_dev ? *a.cand_limit_dev : a.cand_limit;
   int cnt = 0;
   bool packable = true;  // every kept key fits the 64-bit packing (per lane)
+  // The stencil's z-adjacent cells are consecutive cell ids, so their members are one
+  // contiguous range of the cell-ordered arrays: 9 ranges (one per (x, y) column) instead of
+  // 27 cells, scanned as ONE stream of candidates in warp-wide batches (no partly empty
+  // batch per cell).  The order candidates arrive in does not matter: rows are ranked by
+  // the canonical key below.
+  int rb[9], re[9];
+  int nr = 0, total = 0;
   for (int ox = -1; ox <= 1; ++ox) {
     const int x = cx + ox;
     if (x < 0 || x >= a.cdims[0]) continue;
     for (int oy = -1; oy <= 1; ++oy) {
       const int y = cy + oy;
       if (y < 0 || y >= a.cdims[1]) continue;
-      for (int oz = -1; oz <= 1; ++oz) {
-        const int z = cz + oz;
-        if (z < 0 || z >= a.cdims[2]) continue;
-        const int id = (x * a.cdims[1] + y) * a.cdims[2] + z;
-        const int b = a.cell_start[id], e = a.cell_start[id + 1];
-        for (int base = b; base < e; base += 32) {
-          const int j = base + lane;
-          bool keep = false;
-          NbrEntry ent;
-          if (j < e) {
-            const int mj = a.cell_members[j];
-            if (mj != cm && mj < cand_limit) {
-              double d[3];
-              cand_delta(a, j, pc, csh, d);
-              const double r2 = norm2_exact(d[0], d[1], d[2]);
-              if (r2 < a.rc2) {
-                keep = true;
-                ent.j = j;
-                ent.species = a.cs.species[j];
-                const uint64_t rb = static_cast<uint64_t>(__double_as_longlong(r2));
-                const bool ok = rb >= a.kbase && ent.species >= 0 && ent.species < 63;
-                packable = packable && ok;
-                ent.key = (static_cast<uint64_t>(ent.species) << 58) | (rb - a.kbase);
-              }
-            }
-          }
-          const unsigned mask = __ballot_sync(0xffffffffu, keep);
-          if (keep) {
-            const int slot = cnt + __popc(mask & ((1u << lane) - 1u));
-            if (slot < cap) buf[slot] = ent;
-          }
-          cnt += __popc(mask);
+      const int col = (x * a.cdims[1] + y) * a.cdims[2];
+      const int b = a.cell_start[col + max(cz - 1, 0)], e = a.cell_start[col + min(cz + 1, a.cdims[2] - 1) + 1];
+      rb[nr] = b;
+      re[nr] = total + (e - b);  // running end of the stream
+      total += e - b;
+      ++nr;
+    }
+  }
+  int r = 0;  // range of this lane's candidate (advances monotonically)
+  for (int base = 0; base < total; base += 32) {
+    const int t = base + lane;
+    bool keep = false;
+    NbrEntry ent;
+    if (t < total) {
+      while (t >= re[r]) ++r;
+      const int j = rb[r] + t - (r ? re[r - 1] : 0);
+      const int mj = a.cell_members[j];
+      if (mj != cm && mj < cand_limit) {
+        double d[3];
+        cand_delta(a, j, pc, csh, d);
+        const double r2 = norm2_exact(d[0], d[1], d[2]);
+        if (r2 < a.rc2) {
+          keep = true;
+          ent.j = j;
+          ent.species = a.cs.species[j];
+          const uint64_t rbits = static_cast<uint64_t>(__double_as_longlong(r2));
+          const bool ok = rbits >= a.kbase && ent.species >= 0 && ent.species < 63;
+          packable = packable && ok;
+          ent.key = (static_cast<uint64_t>(ent.species) << 58) | (rbits - a.kbase);
         }
       }
     }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int slot = cnt + __popc(mask & ((1u << lane) - 1u));
+      if (slot < cap) buf[slot] = ent;
+    }
+    cnt += __popc(mask);
   }
   __syncwarp();
   if (lane == 0) {
@@ -536,10 +546,32 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
     constexpr int kMaxPer = 32;  // n_max < 1024 (context checks)
     double s2[kMaxPer];
     int rk[kMaxPer];
+    // long lists (rc = 8): the same packed-key ranking one entry at a time, the full
+    // comparison only for a list with a tie or an unpackable key
+    bool fast = __all_sync(0xffffffffu, packable);
+    if (fast) {
+      bool tie = false;
+      for (int i = lane, u = 0; i < cnt; i += 32, ++u) {
+        const uint64_t mk = buf[i].key;
+        int rank = 0, eq = 0;
+        for (int j = 0; j < cnt; ++j) {
+          const uint64_t o = buf[j].key;
+          rank += o < mk;
+          eq += o == mk;
+        }
+        rk[u] = rank;
+        tie = tie || eq != 1;
+      }
+      fast = !__any_sync(0xffffffffu, tie);
+    }
     for (int i = lane, u = 0; i < cnt; i += 32, ++u) {
       const NbrEntry me = buf[i];
       int rank = 0;
-      for (int j = 0; j < cnt; ++j) rank += full_less(a, buf[j], me, pc, csh);
+      if (fast) {
+        rank = rk[u];
+      } else {
+        for (int j = 0; j < cnt; ++j) rank += full_less(a, buf[j], me, pc, csh);
+      }
       out[rank] = a.cell_members[me.j];
       rk[u] = rank;
       if constexpr (ENV) s2[u] = env_row(a, li, rank, me, pc, csh);
