@@ -13,6 +13,8 @@
 // context).  Tensor maps are encoded per call (the buffers they point at may move).
 #include <cuda.h>
 
+#include <cstdio>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tma_gemm.cuh"
@@ -32,6 +34,7 @@ struct FitTmaArgs {
   const float* Y;      // [M][N] tanh activations (FEPI_DTANH)
   int epi;
   int S;               // K slices (split-K): raw partial tiles into C's slice z, epilogue later
+  unsigned long long* prof;  // (TG_PROF builds) [8] clocks: issuer phases 0-6, [7] split wait
 };
 
 template <int NPASS>
@@ -45,6 +48,12 @@ __global__ void __launch_bounds__(tg::kPromoThreads, 1) k_fit_tma(const __grid_c
   if (static_cast<int>(blockIdx.x) >= items) return;
   tg::Ring rg;
   tg::init(rg, ring, ctl, 512);
+#ifdef TG_PROF
+  long long pl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  rg.prof = a.prof ? pl : nullptr;
+  rg.gprof = a.prof ? a.prof + 7 : nullptr;
+  rg.t = clock64();
+#endif
   const int Kc = a.K / a.S;
   for (int w = blockIdx.x; w < items; w += gridDim.x) {
     const int z = w / (tm * tn), t = w - z * tm * tn;
@@ -62,6 +71,10 @@ __global__ void __launch_bounds__(tg::kPromoThreads, 1) k_fit_tma(const __grid_c
                                        vst(&C[o], v);
                                      });
   }
+#ifdef TG_PROF
+  if (a.prof && threadIdx.x == 0)
+    for (int i = 0; i < 7; ++i) atomicAdd(a.prof + i, static_cast<unsigned long long>(pl[i]));
+#endif
   tg::finish(rg);
 }
 
@@ -82,6 +95,15 @@ static void fit_tma(int npass, int n_sm, int M, const int* M_live, int N, int K,
   a.bias = bias;
   a.Y = Y;
   a.epi = epi;
+  a.prof = nullptr;
+#ifdef TG_PROF
+  static unsigned long long* prof = nullptr;
+  if (!prof) {
+    cudaMalloc(&prof, 8 * sizeof(unsigned long long));
+  }
+  cudaMemsetAsync(prof, 0, 8 * sizeof(unsigned long long), st);
+  a.prof = prof;
+#endif
   a.S = ws ? fit_split_k(K) : 1;
   if (a.S > 1) a.C = ws;
   const int tiles = ((M + 127) / 128) * ((N + 127) / 128) * a.S;
@@ -95,6 +117,16 @@ static void fit_tma(int npass, int n_sm, int M, const int* M_live, int N, int K,
     k_fit_tma<1><<<grid, tg::kPromoThreads, smem, st>>>(a);
   }
   count_launch();
+#ifdef TG_PROF
+  unsigned long long h[8];
+  cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  double tot = 0;
+  for (int i = 0; i < 7; ++i) tot += static_cast<double>(h[i]);
+  fprintf(stderr, "[fit_tma M=%d N=%d K=%d S=%d] issuer: wait-ready %.1f%% mma-issue %.1f%% loop %.1f%% drain %.1f%% tmem->smem %.1f%% functor %.1f%% sync %.1f%% | split-wait-landing/issuer-total %.2f\n",
+          M, N, K, a.S, 100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot, 100 * h[3] / tot, 100 * h[4] / tot,
+          100 * h[5] / tot, 100 * h[6] / tot, h[7] / tot);
+#endif
   if (a.S > 1) launch_fit_splitk_sum(M, M_live, N, a.S, ws, C, bias, Y, epi, st);
 }
 

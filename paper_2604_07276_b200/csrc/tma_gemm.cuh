@@ -17,7 +17,7 @@
 // per 8-wide k-step and commits to the stage's mbarrier.
 //
 // Pipeline: a ring of kStages stages of 16 K columns (smem: A raw | B raw | B lo, 8 KB each;
-// TMEM: A raw | A lo, 16 columns each).  Chunk c+kStages-1 is requested as soon as the MMAs
+// TMEM: kAStages stages of A raw | A lo, 16 columns each).  Chunk c+kStages-1 is requested as soon as the MMAs
 // of chunk c are issued (after the MMAs of chunk c-1 have drained its stage), so global
 // latency hides behind three chunks of tensor work; the threads never touch global memory
 // in the main loop.  The chunk counter g runs over all GEMMs of the CTA, so stage and
@@ -42,11 +42,12 @@ namespace tg {
 constexpr int kThreads = 256;        // warp 0 MMA issuer, warps 1-7 split (warp 4 also produces)
 constexpr int kPromoThreads = 384;   // PROMOTE: + warps 8-11 promote
 constexpr int kKC = 16;                  // K columns per chunk: one 64-byte swizzle row
-constexpr int kStages = 4;
+constexpr int kStages = 8;   // shared-memory ring: TMA requests run up to 7 chunks ahead
+constexpr int kAStages = 4;  // TMEM A stages (chunk g uses g % kAStages)
 
 constexpr uint32_t kOpBytes = 8192;      // one operand tile: 128 x 16 fp32
 constexpr uint32_t kStageBytes = 3 * kOpBytes;  // A raw | B raw | B lo
-constexpr uint32_t kRingBytes = kStages * kStageBytes;  // 96 KB; epilogue staging reuses it
+constexpr uint32_t kRingBytes = kStages * kStageBytes;  // 192 KB; epilogue staging reuses it
 constexpr uint32_t kTmemA = 128;         // TMEM column of A stage 0
 constexpr uint32_t kTmemAcc1 = 256;      // PROMOTE: second group accumulator (512 columns)
 constexpr uint32_t kTmemSum = 384;       // PROMOTE: promoted FP32 sum
@@ -290,7 +291,7 @@ __device__ __forceinline__ void gemm(Ring& rg, int M, int N, int K1, const Op& a
         const uint32_t g = g0 + c;
         const int s = g % kStages;
         const int bmn = c < n1 ? b1.mn : b2.mn;
-        const uint32_t ta = rg.tmem + kTmemA + 32u * s;
+        const uint32_t ta = rg.tmem + kTmemA + 32u * (g % kAStages);
         uint32_t acc_t = rg.tmem;
         bool start = c == 0;
         if (PROMOTE > 0) {
@@ -360,11 +361,18 @@ __device__ __forceinline__ void gemm(Ring& rg, int M, int N, int K1, const Op& a
       const int amn = p1 ? a1.mn : a2.mn;
       const uint32_t bbytes = p1 ? b1.bytes : b2.bytes;
       uint8_t* st = rg.base + s * kStageBytes;
-      const uint32_t ta = rg.tmem + kTmemA + 32u * s + lanes;  // A raw; lo at +16
+      const uint32_t ta = rg.tmem + kTmemA + 32u * (g % kAStages) + lanes;  // A raw; lo at +16
 #if defined(TG_TRACE) || defined(TG_PROF)
       const long long tw0 = clock64();
 #endif
       mbar_wait(&ctl->full[s], (g / kStages) & 1u);
+      // the TMEM A stage is shared with chunk g - kAStages: its MMAs must have drained (the
+      // ring's TMA request only waited for chunk g - kStages); earlier GEMMs drained in
+      // their epilogue
+      if (c >= kAStages) {
+        const uint32_t gp = g - kAStages;
+        mbar_wait(&ctl->empty[gp % kStages], (gp / kStages) & 1u);
+      }
       __syncwarp();  // reconverge before the .sync.aligned TMEM stores
 #ifdef TG_PROF
       if (rg.gprof && warp == 1 && lane == 0) atomicAdd(rg.gprof, static_cast<unsigned long long>(clock64() - tw0));
