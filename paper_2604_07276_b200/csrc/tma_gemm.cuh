@@ -197,6 +197,12 @@ __device__ __forceinline__ uint8_t* stage_ptr(const Ring& rg, uint32_t g) { retu
 // measured, tools/micro/tma_test.cu)
 __device__ __forceinline__ float lo1(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 __device__ __forceinline__ float4 lo4(float4 v) { return make_float4(lo1(v.x), lo1(v.y), lo1(v.z), lo1(v.w)); }
+// 3xTF32 split with round-to-nearest hi (tf32_rn, exactly representable, so the tensor core
+// reads it unchanged): |lo| <= 2^-11 |x| with either sign, so the dropped lo*lo term neither
+// reaches 2^-20 nor has a systematic sign, as with the truncated hi of the raw operand
+__device__ __forceinline__ float4 hi4(float4 v) {
+  return make_float4(tc::tf32_rn(v.x), tc::tf32_rn(v.y), tc::tf32_rn(v.z), tc::tf32_rn(v.w));
+}
 
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
@@ -405,22 +411,35 @@ __device__ __forceinline__ void gemm(Ring& rg, int M, int N, int K1, const Op& a
 #endif
       const int h0 = two_h ? 0 : ah;
       __syncwarp();
-      tmem_st8(ta + 8u * h0, v0);
-      if (two_h) tmem_st8(ta + 8u, v1);
       if (NPASS > 1) {
+        // hi = tf32_rn(x) into the A stage, lo = x - hi
+        float h0v[8], h1v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          v0[j] = lo1(v0[j]);
-          v1[j] = lo1(v1[j]);
+          h0v[j] = tc::tf32_rn(v0[j]);
+          h1v[j] = tc::tf32_rn(v1[j]);
+          v0[j] -= h0v[j];
+          v1[j] -= h1v[j];
         }
+        tmem_st8(ta + 8u * h0, h0v);
+        if (two_h) tmem_st8(ta + 8u, h1v);
         tmem_st8(ta + 16u + 8u * h0, v0);
         if (two_h) tmem_st8(ta + 24u, v1);
         __syncwarp();
         if (!two_h) {
+          // B: the landed tile is rewritten in place as hi, its low parts go to the lo tile
+          float4* bh = const_cast<float4*>(br);
 #pragma unroll
           for (int i = 0; i < 3; ++i)
-            if (bt + 192 * i < nb) bl[bt + 192 * i] = lo4(bv[i]);
+            if (bt + 192 * i < nb) {
+              const float4 h = hi4(bv[i]);
+              bh[bt + 192 * i] = h;
+              bl[bt + 192 * i] = make_float4(bv[i].x - h.x, bv[i].y - h.y, bv[i].z - h.z, bv[i].w - h.w);
+            }
         }
+      } else {
+        tmem_st8(ta + 8u * h0, v0);
+        if (two_h) tmem_st8(ta + 8u, v1);
       }
 #ifdef TG_TRACE
       tt[2] = clock64();
