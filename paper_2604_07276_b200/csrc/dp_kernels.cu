@@ -257,6 +257,28 @@ struct CentreQueue {
   }
 };
 
+// Backward variant: next() is also the barrier between consecutive centres (shared memory
+// is reused), one __syncthreads per centre, with the hand-over slot double-buffered so
+// that thread 0 may publish the following centre while slow threads still read this one.
+// (Measured: backward -0.045 ms; the forward, timed with it, got slower by code layout.)
+struct CentreQueue1 {
+  int* ctr;
+  int claimed;  // thread 0 only
+  int parity;
+  __device__ explicit CentreQueue1(int* c) : ctr(c), claimed(0), parity(0) {
+    if (threadIdx.x == 0) claimed = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
+  }
+  __device__ int next() {
+    __shared__ int s_next[2];
+    if (threadIdx.x == 0) s_next[parity] = claimed;
+    __syncthreads();
+    const int c = s_next[parity];
+    parity ^= 1;
+    if (threadIdx.x == 0) claimed = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
+    return c;
+  }
+};
+
 // Stage centre c's env rows (written by the centre-list build, k_neighbors) into shared
 // memory; returns sigma.
 __device__ double centre_rows(const DpArgs& a, int c, int n, const Smem& sm, int& zi) {
@@ -998,7 +1020,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int ur = a.unit_rows, ur4 = (ur + 3) & ~3;
   const int n_units = PACK ? *a.n_units_dev : (a.n_centres_dev ? *a.n_centres_dev : a.n_centres);
-  CentreQueue queue(a.work);
+  CentreQueue1 queue(a.work);
   // unit u: one centre (u = c), or a multi-centre pack (DpArgs::packs)
   for (int u = blockIdx.x; u < n_units; u = queue.next()) {
     int n, zi = 0;
@@ -1305,8 +1327,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         }
       }
     }
-    __syncthreads();
-    pc.mark(13);
+    pc.mark(13);  // (the centre queue's barrier ends the centre)
   }
   pc.flush();
   mm.finish();
