@@ -13,7 +13,8 @@ import sys, json
 for l in sys.stdin:
     if l.startswith('{'):
         d = json.loads(l); k = d['kernel_ms_per_step']
-        print('$v round $round ms/step %.3f fwd %.3f bwd %.3f' % (d['ms_per_step'], k['centre_forward'], k['centre_backward']))
+        fit = sum(v for n, v in k.items() if 'fit' in n)
+        print('$v round $round ms/step %.3f fwd %.3f bwd %.3f fit %.3f' % (d['ms_per_step'], k['centre_forward'], k['centre_backward'], fit))
 "
   done
 done
