@@ -441,36 +441,56 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
       ++nr;
     }
   }
-  int r = 0;  // range of this lane's candidate (advances monotonically)
-  for (int base = 0; base < total; base += 32) {
-    const int t = base + lane;
-    bool keep = false;
-    NbrEntry ent;
-    if (t < total) {
-      while (t >= re[r]) ++r;
-      const int j = rb[r] + t - (r ? re[r - 1] : 0);
-      const int mj = a.cell_members[j];
-      if (mj != cm && mj < cand_limit) {
-        double d[3];
-        cand_delta(a, j, pc, csh, d);
-        const double r2 = norm2_exact(d[0], d[1], d[2]);
+  // Two warp-wide batches per iteration, every load of a candidate issued before any test
+  // (the kernel is bound by the latency of these L2 reads, not by their bytes)
+  int r0 = 0, r1 = 0;  // range of this lane's candidates (each advances monotonically)
+  for (int base = 0; base < total; base += 64) {
+    int jj[2];
+    int mj[2], sj[2], sp[2];
+    double cx_[2], cy_[2], cz_[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int t = base + 32 * h + lane;
+      jj[h] = -1;
+      if (t < total) {
+        int& r = h ? r1 : r0;
+        while (t >= re[r]) ++r;
+        const int j = rb[r] + t - (r ? re[r - 1] : 0);
+        jj[h] = j;
+        mj[h] = a.cell_members[j];
+        cx_[h] = a.cs.x[j];
+        cy_[h] = a.cs.y[j];
+        cz_[h] = a.cs.z[j];
+        sj[h] = a.cs.shift[j];
+        sp[h] = a.cs.species[j];
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      bool keep = false;
+      NbrEntry ent;
+      if (jj[h] >= 0 && mj[h] != cm && mj[h] < cand_limit) {
+        const double d0 = image_delta(cx_[h], pc[0], shift_x(sj[h]) - csh[0], a.L[0]);
+        const double d1 = image_delta(cy_[h], pc[1], shift_y(sj[h]) - csh[1], a.L[1]);
+        const double d2 = image_delta(cz_[h], pc[2], shift_z(sj[h]) - csh[2], a.L[2]);
+        const double r2 = norm2_exact(d0, d1, d2);
         if (r2 < a.rc2) {
           keep = true;
-          ent.j = j;
-          ent.species = a.cs.species[j];
+          ent.j = jj[h];
+          ent.species = sp[h];
           const uint64_t rbits = static_cast<uint64_t>(__double_as_longlong(r2));
           const bool ok = rbits >= a.kbase && ent.species >= 0 && ent.species < 63;
           packable = packable && ok;
           ent.key = (static_cast<uint64_t>(ent.species) << 58) | (rbits - a.kbase);
         }
       }
+      const unsigned mask = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int slot = cnt + __popc(mask & ((1u << lane) - 1u));
+        if (slot < cap) buf[slot] = ent;
+      }
+      cnt += __popc(mask);
     }
-    const unsigned mask = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      const int slot = cnt + __popc(mask & ((1u << lane) - 1u));
-      if (slot < cap) buf[slot] = ent;
-    }
-    cnt += __popc(mask);
   }
   __syncwarp();
   if (lane == 0) {
