@@ -15,7 +15,7 @@ for l in sys.stdin:
         d = json.loads(l); k = d['kernel_ms_per_step']
         fit = sum(v for n, v in k.items() if 'fit' in n)
         nbr = sum(v for n, v in k.items() if 'neighbo' in n or 'nbr' in n)
-        print('$v round $round ms/step %.3f fwd %.3f bwd %.3f fit %.3f nbr %.3f' % (d['ms_per_step'], k['centre_forward'], k['centre_backward'], fit, nbr))
+        print('$v round $round ms/step %.3f fwd %.3f bwd %.3f fit %.3f nbr %.3f gather %.3f' % (d['ms_per_step'], k['centre_forward'], k['centre_backward'], fit, nbr, k.get('force_gather', 0)))
 "
   done
 done
