@@ -400,6 +400,16 @@ __device__ __forceinline__ void env_sigma(const NbrArgs& a, int li, int cnt, con
   if (lane == 0) a.sig[li] = sig;
 }
 
+// rank[u] = number of keys below mine[u] (u < NU; NU warp-uniform, so no per-u guards)
+template <int NU>
+__device__ __forceinline__ void rank_packed(const NbrEntry* buf, int cnt, const uint64_t (&mine)[6], int (&rank)[6]) {
+  for (int j = 0; j < cnt; ++j) {
+    const uint64_t o = buf[j].key;
+#pragma unroll
+    for (int u = 0; u < NU; ++u) rank[u] += o < mine[u];
+  }
+}
+
 // ENV: centre lists, which also write their environment rows (env_row).
 template <bool ENV>
 __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap) {
@@ -425,25 +435,26 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
   // 27 cells, scanned as ONE stream of candidates in warp-wide batches (no partly empty
   // batch per cell).  The order candidates arrive in does not matter: rows are ranked by
   // the canonical key below.
-  int rb[9], re[9];
-  int nr = 0, total = 0;
-  for (int ox = -1; ox <= 1; ++ox) {
-    const int x = cx + ox;
-    if (x < 0 || x >= a.cdims[0]) continue;
-    for (int oy = -1; oy <= 1; ++oy) {
-      const int y = cy + oy;
-      if (y < 0 || y >= a.cdims[1]) continue;
+  // range q = column (ox, oy) = (q / 3 - 1, q % 3 - 1) covers stream positions
+  // [re[q - 1], re[q]) and candidate j = t + dl[q] there; fully unrolled so both arrays stay
+  // in registers (empty for a column outside the grid)
+  int re[9], dl[9];
+  int total = 0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    const int x = cx + q / 3 - 1, y = cy + q % 3 - 1;
+    int b = 0, len = 0;
+    if (x >= 0 && x < a.cdims[0] && y >= 0 && y < a.cdims[1]) {
       const int col = (x * a.cdims[1] + y) * a.cdims[2];
-      const int b = a.cell_start[col + max(cz - 1, 0)], e = a.cell_start[col + min(cz + 1, a.cdims[2] - 1) + 1];
-      rb[nr] = b;
-      re[nr] = total + (e - b);  // running end of the stream
-      total += e - b;
-      ++nr;
+      b = a.cell_start[col + max(cz - 1, 0)];
+      len = a.cell_start[col + min(cz + 1, a.cdims[2] - 1) + 1] - b;
     }
+    dl[q] = b - total;
+    total += len;
+    re[q] = total;
   }
   // Two warp-wide batches per iteration, every load of a candidate issued before any test
   // (the kernel is bound by the latency of these L2 reads, not by their bytes)
-  int r0 = 0, r1 = 0;  // range of this lane's candidates (each advances monotonically)
   for (int base = 0; base < total; base += 64) {
     int jj[2];
     int mj[2], sj[2], sp[2];
@@ -453,9 +464,11 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
       const int t = base + 32 * h + lane;
       jj[h] = -1;
       if (t < total) {
-        int& r = h ? r1 : r0;
-        while (t >= re[r]) ++r;
-        const int j = rb[r] + t - (r ? re[r - 1] : 0);
+        int dj = dl[0];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (t >= re[q]) dj = dl[q + 1];
+        const int j = t + dj;
         jj[h] = j;
         mj[h] = a.cell_members[j];
         cx_[h] = a.cs.x[j];
@@ -520,21 +533,27 @@ __global__ void __launch_bounds__(kNbrWarps * 32) k_neighbors(NbrArgs a, int cap
     }
     bool fast = __all_sync(0xffffffffu, packable);
     if (fast) {
-      int eq = 0;
-      for (int j = 0; j < cnt; ++j) {
-        const uint64_t o = buf[j].key;
-#pragma unroll
-        for (int u = 0; u < kPer; ++u)
-          if (u < nu) {
-            rank[u] += o < mine[u];
-            eq += o == mine[u];
-          }
+      switch (nu) {
+        case 1: rank_packed<1>(buf, cnt, mine, rank); break;
+        case 2: rank_packed<2>(buf, cnt, mine, rank); break;
+        case 3: rank_packed<3>(buf, cnt, mine, rank); break;
+        case 4: rank_packed<4>(buf, cnt, mine, rank); break;
+        case 5: rank_packed<5>(buf, cnt, mine, rank); break;
+        default: rank_packed<6>(buf, cnt, mine, rank); break;
       }
-      // each valid entry meets itself once; padding keys (~0) never equal a packed key
-      int own = 0;
+      // distinct keys give a permutation; an exact key tie gives two entries one rank, so
+      // one of them reads back another entry's tag
+      int* tag = reinterpret_cast<int*>(nbr_smem_raw + static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry)) +
+                 static_cast<size_t>(wid) * cap;
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) own += (lane + 32 * u < cnt);
-      fast = __all_sync(0xffffffffu, eq == own);
+      for (int u = 0; u < kPer; ++u)
+        if (lane + 32 * u < cnt) tag[rank[u]] = lane + 32 * u;
+      __syncwarp();
+      bool ok = true;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (lane + 32 * u < cnt) ok = ok && tag[rank[u]] == lane + 32 * u;
+      fast = __all_sync(0xffffffffu, ok);
     }
     if (!fast) {
       for (int u = 0; u < nu; ++u) {
@@ -611,11 +630,11 @@ void launch_neighbors(const NbrArgs& a, cudaStream_t st) {
   const int cap = ((a.n_max + 1 + 31) / 32) * 32;
   const int grid = (a.n_lists + kNbrWarps - 1) / kNbrWarps;
   if (a.R) {
-    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry);
+    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * (sizeof(NbrEntry) + sizeof(int));
     ensure_smem_attr(reinterpret_cast<const void*>(k_neighbors<true>), smem);
     k_neighbors<true><<<grid, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
   } else {
-    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * sizeof(NbrEntry);
+    const size_t smem = static_cast<size_t>(kNbrWarps) * cap * (sizeof(NbrEntry) + sizeof(int));
     ensure_smem_attr(reinterpret_cast<const void*>(k_neighbors<false>), smem);
     k_neighbors<false><<<grid, kNbrWarps * 32, smem, st>>>(a, cap); count_launch();
   }

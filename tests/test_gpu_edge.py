@@ -85,3 +85,31 @@ def test_empty_one_and_two_atom_systems(ref, models):
         r = ev.compute(pos, sp, box)
         assert abs(r["energy"] - want["energy"]) <= TOL * abs(want["energy"])
         assert np.abs(r["forces"] - want["forces"]).max() <= TOL * max(np.abs(want["forces"]).max(), 1e-12) + 1e-12
+
+
+@pytest.mark.parametrize("half_jitter", [False, True])
+@pytest.mark.parametrize("n_species", [1, 2])
+def test_exact_key_ties_on_a_lattice(ref, models, half_jitter, n_species):
+    """Simple cubic lattice (spacing 2.5 A, exactly representable): every centre sees its 6
+    first and 12 second neighbours at bitwise-equal r^2, so rows hinge on the gid tie-break
+    of the canonical key (deeppot.cpp:141-148).  The centre-list build ranks on a packed
+    (species, r^2) key and must detect these ties and fall back to the full comparison.
+    Half-jittered: ties remain only around unjittered centres."""
+    h, m = models
+    g = np.arange(6) * 2.5
+    pos = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3) + 0.25
+    rng = np.random.default_rng(17)
+    if half_jitter:
+        pos[1::2] += rng.uniform(-0.1, 0.1, size=pos[1::2].shape)
+    sp = (np.arange(len(pos)) % n_species).astype(np.int32)
+    box = np.array([15.0, 15.0, 15.0])
+    gids = (rng.permutation(len(pos)) * 3 + 5).astype(np.int64)
+    rows = rows_by_centre(*ref.center_rows(h, pos, sp, box, gids=gids)[:3])
+    want = ref.evaluate(h, pos, sp, box, gids=gids)
+    ev = nb.DeviceEvaluator(m, n_ranks=1)
+    ev.set_debug(True)
+    r = ev.compute(pos, sp, box, gids=gids)
+    check_rows(ev, 64, rows)
+    assert abs(r["energy"] - want["energy"]) <= TOL * abs(want["energy"])
+    if half_jitter:  # (the perfect lattice's forces cancel to rounding noise)
+        assert rel_err(r["forces"], want["forces"]) <= TOL
