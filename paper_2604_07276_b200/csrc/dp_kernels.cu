@@ -93,6 +93,21 @@ struct Mm {
       tc::gemm<TA, TB, MODE == 1 ? 3 : 1, PROMOTE, NST, EK>(st, M, N, K, A, lda, B, ldb, epi);
     }
   }
+  // run() with A's transposition a runtime flag (one code copy for both orientations)
+  template <bool TB, class Epi>
+  __device__ __forceinline__ void run_dyn(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                                          bool ta, Epi epi) {
+    if constexpr (MODE == 0) {
+      if (ta) bgemm<true, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
+      else bgemm<false, TB>(M, N, K, A, lda, B, ldb, *gs, epi);
+    } else if constexpr (NST == 1) {
+      tc::gemm2_ts<false, TB, false, TB, MODE == 1 ? 3 : 1, 1, false, false, Epi, true>(
+          st, M, N, K, A, lda, B, ldb, 0, A, lda, B, ldb, epi, nullptr, nullptr, ta);
+    } else {
+      if (ta) tc::gemm<true, TB, MODE == 1 ? 3 : 1, 0, NST, 1>(st, M, N, K, A, lda, B, ldb, epi);
+      else tc::gemm<false, TB, MODE == 1 ? 3 : 1, 0, NST, 1>(st, M, N, K, A, lda, B, ldb, epi);
+    }
+  }
   // N = 256 in one SS tile (U = X [A|B]); falls back to run() on the SIMT path.
   template <bool TA, bool TB, bool IMG = false, class Epi>
   __device__ __forceinline__ void run_wide(int M, int N, int K, const float* A, int lda, const float* B, int ldb,
@@ -1184,17 +1199,38 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
       }
       __syncthreads();
       pc.mark(7);
-      // dU_A = dS X ; dU_B = P~^T dY
+      // dU_A = dS X ; dU_B = P~^T dY  (one GEMM call site run twice: half the code)
+#ifdef NB_BWD_TWO_SITES
       mm.template run<false, false>(n, M, n, sl.T, ln, Xl, M,
                           [&](int k, int m, auto v) { vst(&sl.dU[k * M2 + m], v); });
       mm.template run<true, false>(n, M, n, PTl, ln, dY, M,
                          [&](int k, int m, auto v) { vst(&sl.dU[k * M2 + M + m], v); });
+#else
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        float* __restrict__ du = sl.dU + (h ? M : 0);
+        mm.template run_dyn<false>(n, M, n, h ? PTl : sl.T, ln, h ? dY : Xl, M, h != 0,
+                                   [=](int k, int m, auto v) { vst(&du[k * M2 + m], v); });
+      }
+#endif
       __syncthreads();
       pc.mark(9);
       // dX = dY + dS^T U_A + [dU_A | dU_B] [A | B]^T  (both products in one accumulator)
       {
         float* __restrict__ xo = dXn;
         const float* __restrict__ yi = dY;
+#ifndef NB_BWD_TWO_SITES
+        // one call site for every layer: the bottom layer's embedding-output tanh
+        // derivative (dp_core.hpp:580-583), dX0 (1 - X0^2), behind a uniform branch
+        const float* __restrict__ x0 = l == 0 ? X : nullptr;
+        mm.template run2<true, false, false, true, WIMG>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
+                                                   [=](int k, int m, auto v) {
+                                                     auto y = vld(&yi[k * M + m], v) + v;
+                                                     if (x0) y = y * vdtanh(vld(&x0[k * M + m], v));
+                                                     vst(&xo[k * M + m], y);
+                                                   },
+                                                   a.img_abT[l]);
+#else
         if (l > 0) {
           mm.template run2<true, false, false, true, WIMG>(n, M, n, sl.T, ln, Ul, M2, M2, sl.dU, M2, AB, M2, dXn,
                                                      [=](int k, int m, auto v) { vst(&xo[k * M + m], vld(&yi[k * M + m], v) + v); },
@@ -1209,6 +1245,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
                                                      },
                                                      a.img_abT[l]);
         }
+#endif
       }
       __syncthreads();
       pc.mark(11);

@@ -608,12 +608,15 @@ __device__ __forceinline__ void load_arow(const float* __restrict__ A, int lda, 
   }
 }
 
+// DYNA: A's transposition is the runtime flag ta_dyn instead of TA (one code copy serves
+// both orientations: call sites that differ only in it share their instructions).
 template <bool TA, bool TB, bool TA2, bool TB2, int NPASS, int EK = 1, bool IMG1 = false, bool IMG2 = false,
-          class Epi>
+          class Epi, bool DYNA = false>
 __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const float* __restrict__ A, int lda,
                                          const float* __restrict__ B, int ldb, int K2, const float* __restrict__ A2,
                                          int lda2, const float* __restrict__ B2, int ldb2, Epi epi,
-                                         const uint8_t* img1 = nullptr, const uint8_t* img2 = nullptr) {
+                                         const uint8_t* img1 = nullptr, const uint8_t* img2 = nullptr,
+                                         bool ta_dyn = false) {
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   constexpr bool two = NPASS > 1;
@@ -637,7 +640,12 @@ __device__ __forceinline__ void gemm2_ts(State& st, int M, int N, int K, const f
       };
       auto load = [&](int c) {
         if (c < nch1) {
-          load_arow<TA>(A, lda, M, K, m0 + arow, c * kKC + akof, av);
+          if constexpr (DYNA) {
+            if (ta_dyn) load_arow<true>(A, lda, M, K, m0 + arow, c * kKC + akof, av);
+            else load_arow<false>(A, lda, M, K, m0 + arow, c * kKC + akof, av);
+          } else {
+            load_arow<TA>(A, lda, M, K, m0 + arow, c * kKC + akof, av);
+          }
           if (!IMG1) load_chunk<!TB, 4>(B, ldb, N, K, n0, c * kKC, NT, fb);
         } else {
           load_arow<TA2>(A2, lda2, M, K2, m0 + arow, (c - nch1) * kKC + akof, av);
