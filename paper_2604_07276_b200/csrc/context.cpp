@@ -1021,14 +1021,22 @@ void Context::compute_host(long n, const double* pos, const int* types, const in
     }
   }
   compute_device(n, pos_.p, types_.p, gid_.p, box, periodic, out_.p);
-  double head[10];
-  CU(cudaMemcpyAsync(head, out_.p, sizeof head, cudaMemcpyDeviceToHost, st_));
-  if (n && forces) CU(cudaMemcpyAsync(forces, out_.p + 10, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  if (n && atom_energy)
-    CU(cudaMemcpyAsync(atom_energy, out_.p + 10 + 3 * n, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  // the result [E, W(9), F(3n), e_i(n)] comes back in one copy into pinned staging (a
+  // device-to-pageable copy is staged by the driver chunk by chunk), then to the caller
+  const size_t words = 10 + (atom_energy ? 4 : 3) * static_cast<size_t>(n);
+  if (h_out_cap_ < words) {
+    if (h_out_) CU(cudaFreeHost(h_out_));
+    h_out_ = nullptr;
+    h_out_cap_ = 0;
+    CU(cudaMallocHost(reinterpret_cast<void**>(&h_out_), (10 + 4 * static_cast<size_t>(n)) * sizeof(double)));
+    h_out_cap_ = 10 + 4 * static_cast<size_t>(n);
+  }
+  CU(cudaMemcpyAsync(h_out_, out_.p, words * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CU(cudaStreamSynchronize(st_));
-  if (energy) *energy = head[0];
-  if (virial) std::memcpy(virial, head + 1, 9 * sizeof(double));
+  if (energy) *energy = h_out_[0];
+  if (virial) std::memcpy(virial, h_out_ + 1, 9 * sizeof(double));
+  if (n && forces) std::memcpy(forces, h_out_ + 10, 3 * n * sizeof(double));
+  if (n && atom_energy) std::memcpy(atom_energy, h_out_ + 10 + 3 * n, n * sizeof(double));
 }
 
 // ---- pre-split weight images -----------------------------------------------------------
