@@ -1126,7 +1126,58 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
           for (int cc = 0; cc < 4; ++cc) v += sm.dBd[cc * mr + m] * R[cc];
         dY[idx] = v * inm;
       }
-      // dR_k = (X_k dA + X_k[:mr] dB^T) / sqrt(n_max): warp per row, lanes over features
+      // dR_k = (X_k dA + X_k[:mr] dB^T) / sqrt(n_max): warp per row pair (both rows' loads
+      // in flight together), lanes over features; a row's four sums in 6 shuffles (halve
+      // the values per step, then a butterfly: lanes 0, 8, 16, 24 end with x, y, z, w)
+#ifndef NB_DR_ONE_ROW
+      for (int k0 = r0 + wid; k0 < r1; k0 += 2 * nw) {
+        const int k1 = k0 + nw;
+        const bool has1 = k1 < r1;
+        float v[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll 4
+        for (int m = lane; m < M; m += 32) {
+          const float x0 = Xf[k0 * M + m];
+          const float x1 = has1 ? Xf[k1 * M + m] : 0.f;
+          const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];
+          const float xs[2] = {x0, x1};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            v[h][0] += xs[h] * da.x;
+            v[h][1] += xs[h] * da.y;
+            v[h][2] += xs[h] * da.z;
+            v[h][3] += xs[h] * da.w;
+          }
+          if (m < mr) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              v[h][0] += xs[h] * sm.dBd[0 * mr + m];
+              v[h][1] += xs[h] * sm.dBd[1 * mr + m];
+              v[h][2] += xs[h] * sm.dBd[2 * mr + m];
+              v[h][3] += xs[h] * sm.dBd[3 * mr + m];
+            }
+          }
+        }
+        const bool hi16 = lane & 16, hi8 = lane & 8;
+        float b[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float a0 = hi16 ? v[h][2] : v[h][0], a1 = hi16 ? v[h][3] : v[h][1];
+          a0 += __shfl_xor_sync(0xffffffffu, hi16 ? v[h][0] : v[h][2], 16);
+          a1 += __shfl_xor_sync(0xffffffffu, hi16 ? v[h][1] : v[h][3], 16);
+          b[h] = hi8 ? a1 : a0;
+          b[h] += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          b[0] += __shfl_xor_sync(0xffffffffu, b[0], o);
+          b[1] += __shfl_xor_sync(0xffffffffu, b[1], o);
+        }
+        if ((lane & 7) == 0) {
+          reinterpret_cast<float*>(&sm.dR[k0])[lane >> 3] = b[0] * inm;
+          if (has1) reinterpret_cast<float*>(&sm.dR[k1])[lane >> 3] = b[1] * inm;
+        }
+      }
+#else
       for (int k = r0 + wid; k < r1; k += nw) {
         float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;
 #pragma unroll 4
@@ -1150,6 +1201,7 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         v3 = warp_sum(v3);
         if (lane == 0) sm.dR[k] = make_float4(v0 * inm, v1 * inm, v2 * inm, v3 * inm);
       }
+#endif
       if constexpr (PACK) __syncthreads();  // dAd / dBd are reused by the unit's next centre
     }
     __syncthreads();
