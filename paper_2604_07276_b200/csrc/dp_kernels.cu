@@ -836,7 +836,7 @@ __device__ void descriptor(const DpArgs& a, const float* Xf, int r0, int r1, int
     const int kb = r0 + h * nh, ke = min(r1, kb + nh);
     for (int m = threadIdx.x - h * half_threads; m < M; m += half_threads) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 8
+#pragma unroll 16
       for (int k = kb; k < ke; ++k) {
         const float x = Xf[k * M + m];
         const float4 R = sm.R[k];
@@ -864,7 +864,24 @@ __device__ void descriptor(const DpArgs& a, const float* Xf, int r0, int r1, int
     __syncthreads();
   }
   float* D = a.D + static_cast<size_t>(c) * M * mr;
-  for (int idx = threadIdx.x; idx < M * mr; idx += blockDim.x) {
+  // four consecutive q per thread when mr % 4 == 0 (16-byte rows): same products in the
+  // same order as the scalar loop below
+  for (int idx = 4 * threadIdx.x; (mr & 3) == 0 && idx < M * mr; idx += 4 * blockDim.x) {
+    const int m = idx / mr, q0 = idx - m * mr;
+    const float4 am = reinterpret_cast<const float4*>(sm.Ad)[m];
+    const float ac[4] = {am.x, am.y, am.z, am.w};
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const float4 b = *reinterpret_cast<const float4*>(&sm.Bd[cc * mr + q0]);
+      o[0] += ac[cc] * b.x;
+      o[1] += ac[cc] * b.y;
+      o[2] += ac[cc] * b.z;
+      o[3] += ac[cc] * b.w;
+    }
+    *reinterpret_cast<float4*>(&D[idx]) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  for (int idx = threadIdx.x; (mr & 3) != 0 && idx < M * mr; idx += blockDim.x) {
     const int m = idx / mr, q = idx - m * mr;
     float acc = 0.f;
 #pragma unroll
@@ -1350,11 +1367,19 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
             if (k < n) du[u] += dY[k * E0 + o] * w;
           }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float v = warp_sum(du[u]);
-          const int k = k0 + u * nw;
-          if (lane == 0 && k < n) sm.dsx[k] += v;
+        {
+          // the four row sums in 6 shuffles: lanes 0, 8, 16, 24 end with rows u = 0..3
+          const bool hi16 = lane & 16, hi8 = lane & 8;
+          float a0 = hi16 ? du[2] : du[0], a1 = hi16 ? du[3] : du[1];
+          a0 += __shfl_xor_sync(0xffffffffu, hi16 ? du[0] : du[2], 16);
+          a1 += __shfl_xor_sync(0xffffffffu, hi16 ? du[1] : du[3], 16);
+          float b = hi8 ? a1 : a0;
+          b += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+          b += __shfl_xor_sync(0xffffffffu, b, 4);
+          b += __shfl_xor_sync(0xffffffffu, b, 2);
+          b += __shfl_xor_sync(0xffffffffu, b, 1);
+          const int k = k0 + (lane >> 3) * nw;
+          if ((lane & 7) == 0 && k < n) sm.dsx[k] += b;
         }
       }
       __syncthreads();
