@@ -701,72 +701,108 @@ __device__ void bwd_rc_pass(int n, int ln, const float* TS, int ldt, const float
 #pragma unroll
   for (int q = 0; q < 4; ++q) cg[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   float dsg = 0.f;
-  for (int k = wid; k < n; k += nw) {
-    const float4 Rk = sm.R[k];
-    int jb = 0, je = n;
-    if constexpr (PACK) {
-      const int i = sm.rcen[k];
-      jb = sm.pk_off[i];
-      je = sm.pk_off[i + 1];
-      inv_sig = sm.pk_isig[i];
-      dsg = 0.f;
-    }
-    float4 tv = make_float4(0.f, 0.f, 0.f, 0.f), pu = tv;
-    if (act) {
-      tv = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(k) * ldt + j4);
-      pu = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(k) * ln + j4);
-    }
-    const float tq[4] = {tv.x, tv.y, tv.z, tv.w};
-    float pq[4] = {pu.x, pu.y, pu.z, pu.w};
-    float dP[4];
-    float t = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+  // rows in pairs (k, k + nw): both rows' tile and pu loads in flight together and their
+  // shuffle reductions interleaved; every per-lane accumulation keeps the row order
+  for (int k0 = wid; k0 < n; k0 += 2 * nw) {
+    const int kr[2] = {k0, k0 + nw};
+    const bool hv[2] = {true, k0 + nw < n};
+    float4 tv[2], pu[2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool v = j4 + q >= jb && j4 + q < je;
-      const float tt = v ? tq[q] : 0.f;  // the tile and stash hold junk past column n
-      pq[q] = v ? pq[q] : 0.f;
-      const float C = dot4(Rk, Rj[q]);
-      const float pv = sj2[q] * pq[q];
-      dP[q] = tt * C * inv_sig;
-      const float dC = tt * pv * inv_sig;
-      dsg -= dC * C * inv_sig;
-      t += dP[q] * pv;
-      g0 += dC * Rj[q].x;
-      g1 += dC * Rj[q].y;
-      g2 += dC * Rj[q].z;
-      g3 += dC * Rj[q].w;
-      cg[q].x += dC * Rk.x;
-      cg[q].y += dC * Rk.y;
-      cg[q].z += dC * Rk.z;
-      cg[q].w += dC * Rk.w;
+    for (int h = 0; h < 2; ++h) {
+      tv[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      pu[h] = tv[h];
+      if (act && hv[h]) {
+        tv[h] = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(kr[h]) * ldt + j4);
+        pu[h] = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(kr[h]) * ln + j4);
+      }
     }
-    t = warp_sum(t);
-    // the row gate's four sums in 6 shuffles: halve the values per step, then a butterfly;
-    // lanes 0, 8, 16, 24 end up with components x, y, z, w
+    float pq[2][4], dP[2][4], t[2], gg[2][4], isg[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = hv[h] ? kr[h] : k0;
+      const float4 Rk = sm.R[k];
+      int jb = 0, je = n;
+      isg[h] = inv_sig;
+      if constexpr (PACK) {
+        const int i = sm.rcen[k];
+        jb = sm.pk_off[i];
+        je = sm.pk_off[i + 1];
+        isg[h] = sm.pk_isig[i];
+      }
+      const float tq[4] = {tv[h].x, tv[h].y, tv[h].z, tv[h].w};
+      pq[h][0] = pu[h].x;
+      pq[h][1] = pu[h].y;
+      pq[h][2] = pu[h].z;
+      pq[h][3] = pu[h].w;
+      float tt0 = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, dsr = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool v = hv[h] && j4 + q >= jb && j4 + q < je;
+        const float tt = v ? tq[q] : 0.f;  // the tile and stash hold junk past column n
+        pq[h][q] = v ? pq[h][q] : 0.f;
+        const float C = dot4(Rk, Rj[q]);
+        const float pv = sj2[q] * pq[h][q];
+        dP[h][q] = tt * C * isg[h];
+        const float dC = tt * pv * isg[h];
+        if constexpr (PACK) dsr -= dC * C * isg[h];
+        else dsg -= dC * C * isg[h];
+        tt0 += dP[h][q] * pv;
+        g0 += dC * Rj[q].x;
+        g1 += dC * Rj[q].y;
+        g2 += dC * Rj[q].z;
+        g3 += dC * Rj[q].w;
+        cg[q].x += dC * Rk.x;
+        cg[q].y += dC * Rk.y;
+        cg[q].z += dC * Rk.z;
+        cg[q].w += dC * Rk.w;
+      }
+      if constexpr (PACK) {
+        dsr = warp_sum(dsr);
+        if (lane == 0 && hv[h]) sm.rowpart[kr[h]] = dsr;
+      }
+      t[h] = tt0;
+      gg[h][0] = g0;
+      gg[h][1] = g1;
+      gg[h][2] = g2;
+      gg[h][3] = g3;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t[0] += __shfl_xor_sync(0xffffffffu, t[0], o);
+      t[1] += __shfl_xor_sync(0xffffffffu, t[1], o);
+    }
     {
-      const bool hi16 = lane & 16;
-      float a0 = hi16 ? g2 : g0, a1 = hi16 ? g3 : g1;
-      a0 += __shfl_xor_sync(0xffffffffu, hi16 ? g0 : g2, 16);
-      a1 += __shfl_xor_sync(0xffffffffu, hi16 ? g1 : g3, 16);
-      const bool hi8 = lane & 8;
-      float b = hi8 ? a1 : a0;
-      b += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
-      b += __shfl_xor_sync(0xffffffffu, b, 4);
-      b += __shfl_xor_sync(0xffffffffu, b, 2);
-      b += __shfl_xor_sync(0xffffffffu, b, 1);
-      if ((lane & 7) == 0) reinterpret_cast<float*>(&sm.dR[k])[lane >> 3] += b;
-    }
-    float ds[4];
+      const bool hi16 = lane & 16, hi8 = lane & 8;
+      float b[2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float dpt = dP[q] - t;
-      cw[q] += pq[q] * dpt;
-      ds[q] = sj2[q] * pq[q] * dpt;
+      for (int h = 0; h < 2; ++h) {
+        float a0 = hi16 ? gg[h][2] : gg[h][0], a1 = hi16 ? gg[h][3] : gg[h][1];
+        a0 += __shfl_xor_sync(0xffffffffu, hi16 ? gg[h][0] : gg[h][2], 16);
+        a1 += __shfl_xor_sync(0xffffffffu, hi16 ? gg[h][1] : gg[h][3], 16);
+        b[h] = hi8 ? a1 : a0;
+        b[h] += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        b[0] += __shfl_xor_sync(0xffffffffu, b[0], o);
+        b[1] += __shfl_xor_sync(0xffffffffu, b[1], o);
+      }
+      if ((lane & 7) == 0) {
+        reinterpret_cast<float*>(&sm.dR[kr[0]])[lane >> 3] += b[0];
+        if (hv[1]) reinterpret_cast<float*>(&sm.dR[kr[1]])[lane >> 3] += b[1];
+      }
     }
-    if (act) *reinterpret_cast<float4*>(DS + static_cast<size_t>(k) * ln + j4) = make_float4(ds[0], ds[1], ds[2], ds[3]);
-    if constexpr (PACK) {
-      dsg = warp_sum(dsg);
-      if (lane == 0) sm.rowpart[k] = dsg;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float ds[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float dpt = dP[h][q] - t[h];
+        cw[q] += pq[h][q] * dpt;
+        ds[q] = sj2[q] * pq[h][q] * dpt;
+      }
+      if (act && hv[h])
+        *reinterpret_cast<float4*>(DS + static_cast<size_t>(kr[h]) * ln + j4) = make_float4(ds[0], ds[1], ds[2], ds[3]);
     }
   }
   if constexpr (!PACK) {
