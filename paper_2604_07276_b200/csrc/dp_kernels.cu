@@ -480,50 +480,79 @@ __device__ void softmax_gate(int n, int ln, const float* S, int lds, float* PU, 
 __device__ void bwd_row_pass(int n, int ln, const float* TS, int ldt, const float* __restrict__ PU, float inv_sig,
                              const Smem& sm) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = wid; k < n; k += nw) {
-    const float4 Rk = sm.R[k];
-    float t = 0.f, dsg = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f;
+  // rows in pairs (k, k + nw): both rows' tile and pu loads in flight together, their
+  // reductions interleaved, the gate's four sums in 6 shuffles (lanes 0, 8, 16, 24 end with
+  // x, y, z, w); every per-lane accumulation keeps the column order
+  for (int k0 = wid; k0 < n; k0 += 2 * nw) {
+    const bool hv1 = k0 + nw < n;
+    const int kr[2] = {k0, hv1 ? k0 + nw : k0};
+    const float4 Rk[2] = {sm.R[kr[0]], sm.R[kr[1]]};
+    float t[2] = {0.f, 0.f}, dsg[2] = {0.f, 0.f};
+    float g[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     for (int j4 = 4 * lane; j4 < n; j4 += 128) {
-      const float4 tv = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(k) * ldt + j4);
-      const float4 pu = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(k) * ln + j4);
-      const float tq[4] = {tv.x, tv.y, tv.z, tv.w};
-      const float pq[4] = {pu.x, pu.y, pu.z, pu.w};
+      float4 tv[2], pu[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = j4 + q;
-        if (j < n) {
-          const float sj = sm.s[j];
-          const float4 Rj = sm.R[j];
-          const float C = dot4(Rk, Rj);
-          const float pv = sj * sj * pq[q];
-          const float dP = tq[q] * C * inv_sig;
-          const float dC = tq[q] * pv * inv_sig;
-          dsg -= dC * C * inv_sig;
-          t += dP * pv;
-          g0 += dC * Rj.x;
-          g1 += dC * Rj.y;
-          g2 += dC * Rj.z;
-          g3 += dC * Rj.w;
+      for (int h = 0; h < 2; ++h) {
+        tv[h] = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(kr[h]) * ldt + j4);
+        pu[h] = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(kr[h]) * ln + j4);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float tq[4] = {tv[h].x, tv[h].y, tv[h].z, tv[h].w};
+        const float pq[4] = {pu[h].x, pu[h].y, pu[h].z, pu[h].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j4 + q;
+          if (j < n) {
+            const float sj = sm.s[j];
+            const float4 Rj = sm.R[j];
+            const float C = dot4(Rk[h], Rj);
+            const float pv = sj * sj * pq[q];
+            const float dP = tq[q] * C * inv_sig;
+            const float dC = tq[q] * pv * inv_sig;
+            dsg[h] -= dC * C * inv_sig;
+            t[h] += dP * pv;
+            g[h][0] += dC * Rj.x;
+            g[h][1] += dC * Rj.y;
+            g[h][2] += dC * Rj.z;
+            g[h][3] += dC * Rj.w;
+          }
         }
       }
     }
-    t = warp_sum(t);
-    dsg = warp_sum(dsg);
-    g0 = warp_sum(g0);
-    g1 = warp_sum(g1);
-    g2 = warp_sum(g2);
-    g3 = warp_sum(g3);
-    if (lane == 0) {
-      sm.t[k] = t;
-      sm.rowpart[k] = dsg;
-      float4 r = sm.dR[k];
-      r.x += g0;
-      r.y += g1;
-      r.z += g2;
-      r.w += g3;
-      sm.dR[k] = r;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t[0] += __shfl_xor_sync(0xffffffffu, t[0], o);
+      t[1] += __shfl_xor_sync(0xffffffffu, t[1], o);
+      dsg[0] += __shfl_xor_sync(0xffffffffu, dsg[0], o);
+      dsg[1] += __shfl_xor_sync(0xffffffffu, dsg[1], o);
+    }
+    const bool hi16 = lane & 16, hi8 = lane & 8;
+    float b[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float a0 = hi16 ? g[h][2] : g[h][0], a1 = hi16 ? g[h][3] : g[h][1];
+      a0 += __shfl_xor_sync(0xffffffffu, hi16 ? g[h][0] : g[h][2], 16);
+      a1 += __shfl_xor_sync(0xffffffffu, hi16 ? g[h][1] : g[h][3], 16);
+      b[h] = hi8 ? a1 : a0;
+      b[h] += __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      b[0] += __shfl_xor_sync(0xffffffffu, b[0], o);
+      b[1] += __shfl_xor_sync(0xffffffffu, b[1], o);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !hv1) break;
+      if (lane == 0) {
+        sm.t[kr[h]] = t[h];
+        sm.rowpart[kr[h]] = dsg[h];
+      }
+      if ((lane & 7) == 0) reinterpret_cast<float*>(&sm.dR[kr[h]])[lane >> 3] += b[h];
     }
   }
+
 }
 
 // Column pass (thread per key column j and k-half, coalesced across threads), after the
