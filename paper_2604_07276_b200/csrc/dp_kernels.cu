@@ -390,6 +390,61 @@ __device__ void softmax_gate_rc(int n, int ln, const float* S, int lds, float* P
     s2[t] = j < n ? sm.s[j] * sm.s[j] : 0.f;
     Rj[t] = j < n ? sm.R[j] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  if constexpr (C == 8 && !PACK) {
+    // n > 128 (scores in global memory): rows in pairs, both rows' score loads in flight
+    // and their max / sum butterflies interleaved; per-lane order kept
+    for (int k0 = wid; k0 < n; k0 += 2 * nw) {
+      const bool hv1 = k0 + nw < n;
+      const int kr[2] = {k0, hv1 ? k0 + nw : k0};
+      float e[2][C], mx[2] = {-FLT_MAX, -FLT_MAX}, den[2] = {0.f, 0.f};
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < C; ++t) {
+          const int j = lane + 32 * t;
+          e[h][t] = j < n ? S[static_cast<size_t>(kr[h]) * lds + j] : -FLT_MAX;
+        }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < C; ++t) mx[h] = fmaxf(mx[h], e[h][t]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx[0] = fmaxf(mx[0], __shfl_xor_sync(0xffffffffu, mx[0], o));
+        mx[1] = fmaxf(mx[1], __shfl_xor_sync(0xffffffffu, mx[1], o));
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < C; ++t) {
+          const int j = lane + 32 * t;
+          e[h][t] = j < n ? __expf(e[h][t] - mx[h]) : 0.f;
+          den[h] += s2[t] * e[h][t];
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        den[0] += __shfl_xor_sync(0xffffffffu, den[0], o);
+        den[1] += __shfl_xor_sync(0xffffffffu, den[1], o);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !hv1) break;
+        const int k = kr[h];
+        const float inv = den[h] > 0.f ? 1.0f / den[h] : 0.f;
+        const float4 Rk = sm.R[k];
+#pragma unroll
+        for (int t = 0; t < C; ++t) {
+          const int j = lane + 32 * t;
+          if (j < n) {
+            const float pu = e[h][t] * inv;
+            if (PU) PU[static_cast<size_t>(k) * ln + j] = pu;
+            PT[static_cast<size_t>(k) * ln + j] = s2[t] * pu * (dot4(Rk, Rj[t]) * inv_sig);
+          }
+        }
+      }
+    }
+    return;
+  }
   for (int k = wid; k < n; k += nw) {
     // the row's scores, all loads issued before the reductions
     float cur[C];
