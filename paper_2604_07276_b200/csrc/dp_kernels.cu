@@ -701,30 +701,43 @@ __device__ void bwd_colwin_pass(int n, int ln, const float* TS, int ldt, const f
 #pragma unroll
     for (int q = 0; q < 4; ++q) cg[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (act) {
-      for (int k = wid; k < n; k += nw) {
-        const float4 Rk = sm.R[k];
-        const float tk = sm.t[k];
-        const float4 tv = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(k) * ldt + j4);
-        const float4 pu = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(k) * ln + j4);
-        const float tq[4] = {tv.x, tv.y, tv.z, tv.w};
-        const float pq[4] = {pu.x, pu.y, pu.z, pu.w};
-        float ds[4];
+      // rows in pairs: both rows' loads before either row's store (DS aliases TS, so the
+      // compiler cannot move a later row's loads above an earlier row's store itself)
+      for (int k0 = wid; k0 < n; k0 += 2 * nw) {
+        const bool hv1 = k0 + nw < n;
+        const int kr[2] = {k0, hv1 ? k0 + nw : k0};
+        float4 tv2[2], pu2[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const bool v = j4 + q < n;  // the tile and stash hold junk past column n
-          const float tt = v ? tq[q] : 0.f, pp = v ? pq[q] : 0.f;
-          const float C = dot4(Rk, Rj[q]);
-          const float dP = tt * C * inv_sig;
-          const float dC = tt * (sj2[q] * pp) * inv_sig;
-          const float dpt = dP - tk;
-          cw[q] += pp * dpt;
-          ds[q] = sj2[q] * pp * dpt;
-          cg[q].x += dC * Rk.x;
-          cg[q].y += dC * Rk.y;
-          cg[q].z += dC * Rk.z;
-          cg[q].w += dC * Rk.w;
+        for (int h = 0; h < 2; ++h) {
+          tv2[h] = *reinterpret_cast<const float4*>(TS + static_cast<size_t>(kr[h]) * ldt + j4);
+          pu2[h] = *reinterpret_cast<const float4*>(PU + static_cast<size_t>(kr[h]) * ln + j4);
         }
-        *reinterpret_cast<float4*>(DS + static_cast<size_t>(k) * ln + j4) = make_float4(ds[0], ds[1], ds[2], ds[3]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !hv1) break;
+          const int k = kr[h];
+          const float4 Rk = sm.R[k];
+          const float tk = sm.t[k];
+          const float tq[4] = {tv2[h].x, tv2[h].y, tv2[h].z, tv2[h].w};
+          const float pq[4] = {pu2[h].x, pu2[h].y, pu2[h].z, pu2[h].w};
+          float ds[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool v = j4 + q < n;  // the tile and stash hold junk past column n
+            const float tt = v ? tq[q] : 0.f, pp = v ? pq[q] : 0.f;
+            const float C = dot4(Rk, Rj[q]);
+            const float dP = tt * C * inv_sig;
+            const float dC = tt * (sj2[q] * pp) * inv_sig;
+            const float dpt = dP - tk;
+            cw[q] += pp * dpt;
+            ds[q] = sj2[q] * pp * dpt;
+            cg[q].x += dC * Rk.x;
+            cg[q].y += dC * Rk.y;
+            cg[q].z += dC * Rk.z;
+            cg[q].w += dC * Rk.w;
+          }
+          *reinterpret_cast<float4*>(DS + static_cast<size_t>(k) * ln + j4) = make_float4(ds[0], ds[1], ds[2], ds[3]);
+        }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
