@@ -1263,6 +1263,31 @@ __global__ void __launch_bounds__(256, 2) k_centre_backward(const __grid_constan
         }
         __syncthreads();
       }
+      if (static_cast<int>(blockDim.x) % M == 0) {
+        // a thread keeps one feature m for all its rows: dA[m], dB[:, m] read once, no
+        // index division; per element the same operations in the same order
+        const int m = threadIdx.x % M, rstep = blockDim.x / M;
+        const float4 da = reinterpret_cast<const float4*>(sm.dAd)[m];
+        const bool hb = m < mr;
+        float db[4] = {0.f, 0.f, 0.f, 0.f};
+        if (hb)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) db[cc] = sm.dBd[cc * mr + m];
+        for (int k = r0 + static_cast<int>(threadIdx.x) / M; k < r1; k += rstep) {
+          const float4 Rk = sm.R[k];
+          float v = da.x * Rk.x;
+          v += da.y * Rk.y;
+          v += da.z * Rk.z;
+          v += da.w * Rk.w;
+          if (hb) {
+            v += db[0] * Rk.x;
+            v += db[1] * Rk.y;
+            v += db[2] * Rk.z;
+            v += db[3] * Rk.w;
+          }
+          dY[k * M + m] = v * inm;
+        }
+      } else
       for (int idx = r0 * M + threadIdx.x; idx < r1 * M; idx += blockDim.x) {
         const int k = idx / M, m = idx - k * M;
         const float* R = reinterpret_cast<const float*>(&sm.R[k]);
