@@ -353,6 +353,16 @@ __device__ void embed_forward(MmT& mm, const DpArgs& a, int n, int zi, const Sme
                               float* out) {
   const int E0 = a.edims[0];
   float* cur = (a.n_embed == 1) ? out : emb;
+  if (static_cast<int>(blockDim.x) % E0 == 0) {
+    // one fixed output o per thread for all its rows: w0[o] read once, no index division
+    const int o = threadIdx.x % E0, rstep = blockDim.x / E0;
+    const float w = a.w0[o];
+    for (int k = static_cast<int>(threadIdx.x) / E0; k < n; k += rstep) {
+      const int zc = PACK ? sm.pk_zi[sm.rcen[k]] : zi;  // the row's centre species
+      const float v = fmaf(sm.s[k], w, a.ctab[(static_cast<size_t>(sm.z[k]) * a.ns + zc) * E0 + o]);
+      cur[k * E0 + o] = tanhf(v);
+    }
+  } else
   for (int idx = threadIdx.x; idx < n * E0; idx += blockDim.x) {
     const int k = idx / E0, o = idx - k * E0;
     const int zc = PACK ? sm.pk_zi[sm.rcen[k]] : zi;  // the row's centre species
